@@ -1,0 +1,387 @@
+"""Benchmark of the VL-Cache compress + compressed-decode hot path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--batch B]
+
+One step = one pass of the path over one batch of synthetic prompts at the
+LLaVA-1.6-Mistral-7B shapes of BASELINE.json configs[1]: 32 layers, 32 Q / 8
+KV heads, d = 128, m = 2,960 prompt tokens (16 text + 2,880 visual + 64
+post-vision), tau = 64, alpha = 0.1, then 99 decode steps (100 output tokens,
+reference bench.py:361).  Inputs come from the reference's own synthetic
+generator (restated in paper_2410_23317_b200/trace.py), rounded to bf16.
+
+value  = generated tokens / s over the whole step (compress + 99 decode steps),
+         all ranks (weak scaling: each rank owns its own prompts).
+e2e    = the same through the public API with host (pinned) inputs: H2D of the
+         step's Q/K/V inside the timed region, D2H of the kept counts and the
+         last decode output.
+roofline: the dominant kernel of the step (K5 decode, HBM-bound, unless K1
+         dominates), from CUDA events; cold-L2 per-launch K5 timings.
+cpu_baseline: the reference's own compiled kernels (oracle/_ref) or the C
+         oracle, on a bounded sample of the same workload, all host threads.
+--impl reference: that CPU arm as the headline line (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress ms/prompt + compressed-decode tokens/s @LLaVA-1.6-7B, 10% budget, % HBM roofline"
+CFG = dict(layers=32, q_heads=32, kv_heads=8, head_dim=128, prompt_len=2960, tau=64, alpha=0.1,
+           n_out=100, p=0.01, recent=0.10)
+L2_FLUSH_BYTES = 512 << 20   # > 126 MB L2: written between timed steps
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk["hbm_gbs"], pk["bf16_tflops"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, "fallback"
+
+
+def synth_inputs(batch, seed0, w):
+    """bf16-rounded host arrays [B, L, H, rows, d] from the reference generator."""
+    from paper_2410_23317_b200.trace import GenSpec, iter_layers, round_to_bf16, synthesize_values
+
+    c = CFG
+    qw, qd, ks, vs = [], [], [], []
+    for b in range(batch):
+        spec = GenSpec(num_layers=c["layers"], num_query_heads=c["q_heads"], num_kv_heads=c["kv_heads"],
+                       head_dim=c["head_dim"], prompt_len=c["prompt_len"], post_vision_len=c["tau"],
+                       decode_len=c["n_out"] - 1, seed=seed0 + b)
+        k_l, qw_l, qd_l = [], [], []
+        for k, q in iter_layers(spec, keep_prompt_rows=w):
+            k_l.append(round_to_bf16(k))
+            q = round_to_bf16(q)
+            qw_l.append(q[:, :w])
+            qd_l.append(q[:, w:])
+        ks.append(np.stack(k_l))
+        qw.append(np.stack(qw_l))
+        qd.append(np.stack(qd_l))
+        vs.append(np.stack([round_to_bf16(v) for v in synthesize_values(spec)]))
+    return np.stack(qw), np.stack(qd), np.stack(ks), np.stack(vs)
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling (NVML) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - NVML optional
+            self.nv = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------- CPU arm
+def cpu_path(sample_layers, threads, kernels_kind, inputs=None):
+    """Time the reference CPU path (fused compression pass + 99-step compressed
+    decode, reference bench.py:245-372) on `sample_layers` of the 32 layers;
+    returns (compress_s, decode_s) extrapolated to all layers, and the sample
+    description.  The stats loop uses `threads` host threads (the kernel
+    releases the GIL, reference _core.pyx:234)."""
+    from oracle import oracle as O
+
+    c = CFG
+    kern = O.Kernels(kernels_kind)
+    if inputs is None:
+        inputs = synth_inputs(1, 0, c["tau"])
+    qw, qd, ks, vs = (x[0] for x in inputs)
+    g = c["q_heads"] // c["kv_heads"]
+    L = c["layers"]
+    layers = list(range(sample_layers))
+    as_list = lambda a: [np.ascontiguousarray(a[l], dtype=np.float32) for l in range(L)]  # noqa: E731
+    qw_l, qd_l, k_l, v_l = as_list(qw), as_list(qd), as_list(ks), as_list(vs)
+    t0 = time.perf_counter()
+    res = O.compression_pass(qw_l, k_l, c["prompt_len"], g, kernels=kern, threads=threads, layers=layers)
+    # eviction for the sampled layers with the budgets the full pass would give
+    # (the allocation itself is O(L) and negligible)
+    kept = [[O.evict(res["scores"][l, kv], max(1, int(math.ceil(c["alpha"] * c["prompt_len"]))),
+                     c["recent"]) for kv in range(c["kv_heads"])] if l in layers else None for l in range(L)]
+    t1 = time.perf_counter()
+    O.decode_sequence(qd_l, k_l, v_l, kept, c["prompt_len"], g, c["n_out"] - 1, kernels=kern,
+                      layers=layers, collect=False)
+    t2 = time.perf_counter()
+    scale = L / sample_layers
+    desc = (f"{sample_layers} of {L} layers (all heads), fused stats+alloc+evict pass on {threads} "
+            f"threads + 99-step compressed decode, extrapolated x{scale:g} to the full prompt")
+    return (t1 - t0) * scale, (t2 - t1) * scale, desc
+
+
+def cpu_kind():
+    from oracle import oracle as O
+
+    return "reference" if O.ref_module() is not None else "port"
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    kind = cpu_kind()
+    inputs = synth_inputs(1, 0, CFG["tau"])
+    sample = 2
+    for _ in range(args.warmup):
+        cpu_path(sample, threads, "reference" if kind == "reference" else "oracle", inputs)
+    times = []
+    for _ in range(args.steps):
+        tc, td, desc = cpu_path(sample, threads, "reference" if kind == "reference" else "oracle", inputs)
+        times.append((tc, td))
+    tc = statistics.median(t[0] for t in times)
+    td = statistics.median(t[1] for t in times)
+    step = tc + td
+    value = (CFG["n_out"] - 1) / step
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference generator, bf16-rounded)",
+        "config": {"workload": "llava-1.6-mistral-7b shapes: L32 Hq32 Hkv8 d128 m2960 tau64 alpha0.1 "
+                               "batch1, 99 decode steps", "global_batch": 1, "seq_len": CFG["prompt_len"]},
+        "compress_ms_per_prompt": tc * 1e3, "decode_tokens_per_s": (CFG["n_out"] - 1) / td,
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": threads, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- GPU arm
+def decode_bytes_per_step(kept_counts, step):
+    """Algorithmic HBM bytes of one K5 launch: every cached K
+    and V row of every slot read once (k + step + 1 rows), the appended row
+    read + written, Q read, output written."""
+    c = CFG
+    d, hkv, hq = c["head_dim"], c["kv_heads"], c["q_heads"]
+    rows = hkv * (kept_counts + step + 1).sum()
+    return (rows * d * 2 * 2 + kept_counts.size * hkv * d * 2 * 2 * 2
+            + kept_counts.size * hq * d * (2 + 4))
+
+
+def k1_flops(batch):
+    c = CFG
+    m, tau = c["prompt_len"], c["tau"]
+    causal = tau * (m - tau) + tau * (tau + 1) // 2
+    return 2 * c["head_dim"] * c["q_heads"] * causal * c["layers"] * batch
+
+
+def run_gpu_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_23317_b200.engine import Shape, VLCache
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CFG
+    B, n_dec = args.batch, c["n_out"] - 1
+    qw, qd, ks, vs = synth_inputs(B, seed0=rank * B, w=c["tau"])
+    pin = lambda a: torch.from_numpy(a).to(torch.bfloat16).pin_memory()  # noqa: E731
+    h_qw, h_qd, h_k, h_v = pin(qw), pin(qd), pin(ks), pin(vs)
+    d_qw, d_qd, d_k, d_v = (t.cuda() for t in (h_qw, h_qd, h_k, h_v))
+    shape = Shape(B, c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], c["prompt_len"], c["tau"])
+    eng = VLCache(shape, alpha=c["alpha"], p=c["p"], recent_frac=c["recent"], decode_steps=n_dec)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def step(timers=None):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timers is not None else None
+        if e: e[0].record(st)
+        eng.score_stats(d_qw, d_k)
+        if e: e[1].record(st)
+        eng.allocate(); eng.select(); eng.gather(d_k, d_v)
+        if e: e[2].record(st)
+        eng.decode(d_qd, d_k, d_v, graph=True)
+        if e: e[3].record(st)
+        if timers is not None:
+            timers.append(e)
+
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step([])
+    torch.cuda.synchronize()
+    eng.check()
+    timers = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()   # L2 flush between timed steps (outside the events)
+            step(timers)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    k1 = [t[0].elapsed_time(t[1]) for t in timers]
+    k234 = [t[1].elapsed_time(t[2]) for t in timers]
+    dec = [t[2].elapsed_time(t[3]) for t in timers]
+    step_ms = float(np.mean([a + b + d for a, b, d in zip(k1, k234, dec)]))
+    t_step = torch.tensor([step_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
+    step_ms = float(t_step.item())
+    tokens = B * n_dec * world
+    value = tokens / (step_ms / 1e3)
+
+    # cold-L2 per-launch K5 timing (HBM roofline of the dominant kernel)
+    counts = eng.kept_counts.view(B, c["layers"]).cpu().numpy()
+    eng.score_stats(d_qw, d_k); eng.allocate(); eng.select(); eng.gather(d_k, d_v)
+    per = []
+    for s_ in range(n_dec):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        eng.decode_step(d_qd, d_k, d_v, s_)
+        b.record(st)
+        per.append((a, b))
+    torch.cuda.synchronize()
+    k5_ms = [a.elapsed_time(b) for a, b in per]
+    k5_bytes = [decode_bytes_per_step(counts.reshape(-1), s_) for s_ in range(n_dec)]
+    hbm_peak, tc_peak, src = peaks()
+    k5_achieved = float(np.mean([by / (ms / 1e3) for by, ms in zip(k5_bytes, k5_ms)])) / 1e9
+    k1_ms = float(np.mean(k1))
+    k1_tflops = k1_flops(B) / (k1_ms / 1e3) / 1e12
+    dec_ms = float(np.mean(dec))
+    if dec_ms >= k1_ms:
+        roof = {"kernel": "K5 decode_step (cold L2, per launch)", "bound": "hbm", "achieved": k5_achieved,
+                "peak": hbm_peak, "unit": "GB/s", "frac": k5_achieved / hbm_peak, "traffic": None,
+                "peak_source": src, "bytes_per_launch": float(np.mean(k5_bytes)),
+                "launch_us": float(np.mean(k5_ms)) * 1e3}
+    else:
+        roof = {"kernel": "K1 score_stats", "bound": "tensor", "achieved": k1_tflops, "peak": tc_peak,
+                "unit": "TFLOP/s", "frac": k1_tflops / tc_peak, "traffic": None, "peak_source": src,
+                "flops_per_launch": k1_flops(B), "launch_us": k1_ms * 1e3}
+
+    # e2e through the public API with host buffers
+    e2e_ms = []
+    h2d = sum(t.numel() * 2 for t in (h_qw, h_qd, h_k, h_v))
+    d2h = eng.kept_counts.numel() * 8 + eng.out.numel() * 4
+    out_h = torch.empty(eng.out.numel(), dtype=torch.float32).pin_memory()
+    cnt_h = torch.empty(eng.kept_counts.numel(), dtype=torch.int64).pin_memory()
+    for i in range(max(3, args.warmup) + args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for dst, src_ in ((d_qw, h_qw), (d_qd, h_qd), (d_k, h_k), (d_v, h_v)):
+            dst.copy_(src_, non_blocking=True)
+        step()
+        cnt_h.copy_(eng.kept_counts, non_blocking=True)
+        out_h.copy_(eng.out, non_blocking=True)
+        b.record(st)
+        torch.cuda.synchronize()
+        if i >= max(3, args.warmup):
+            e2e_ms.append(a.elapsed_time(b))
+    t_e2e = torch.tensor([float(np.mean(e2e_ms))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = tokens / (float(t_e2e.item()) / 1e3)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (reference trace generator, bf16-rounded; seed = rank*B + b)",
+        "config": {"workload": "llava-1.6-mistral-7b shapes: L32 Hq32 Hkv8 d128 m2960 (16+2880+64) "
+                               "tau64 alpha0.1, 99 decode steps", "global_batch": B * world,
+                   "seq_len": c["prompt_len"], "parallelism": f"batch-sharded x{world} (no collective)",
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "compress_ms_per_prompt": (float(np.mean(k1)) + float(np.mean(k234))) / B,
+        "k1_ms": k1_ms, "k234_ms": float(np.mean(k234)), "decode_ms_99_steps": dec_ms,
+        "decode_tokens_per_s": B * n_dec * world / (dec_ms / 1e3),
+        "k1_tensor_tflops": k1_tflops, "k1_tensor_frac": k1_tflops / tc_peak,
+        "roofline": roof,
+        "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": args.steps * (4 + n_dec),
+        "clocks": clk.summary(),
+        "kept_tokens_per_layer_mean": float(counts.mean()),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        kind = cpu_kind()
+        tc, td, desc = cpu_path(args.cpu_layers, threads, "reference" if kind == "reference" else "oracle",
+                                (qw[:1], qd[:1], ks[:1], vs[:1]))
+        line["cpu_baseline"] = {"value": n_dec / (tc + td), "unit": "tok/s", "cores": threads,
+                                "kind": kind, "sample": desc, "compress_ms_per_prompt": tc * 1e3,
+                                "decode_tokens_per_s": n_dec / td}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--batch", type=int, default=1, help="prompts per GPU")
+    ap.add_argument("--cpu-layers", type=int, default=8, help="layers in the CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

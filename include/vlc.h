@@ -1,0 +1,143 @@
+/*
+ * vlc.h -- C-ABI of the B200 (sm_100a) VL-Cache compress + compressed-decode path.
+ *
+ * Shared library: paper_2410_23317_b200/libvlc_b200.so (built by
+ * __graft_entry__.build()).  Plain pointers and sizes only; every pointer
+ * argument is DEVICE memory owned by the caller unless stated otherwise, every
+ * call is ordered on `stream` (a cudaStream_t / CUstream, NULL = legacy
+ * default) and returns 0 or a negative VLC_E* code; vlc_last_error() gives the
+ * message of the last failure on the calling thread.  No global mutable
+ * state: calls on different streams may run concurrently.
+ *
+ * It replaces the reference's kernel seam `vlcache._kernels`
+ * (reference pkg/src/vlcache/_kernels/__init__.py:10-27, which binds
+ * _core.stats_tiled / _core.decode_step), batched over every
+ * (batch b, layer l, KV head kv) "slot" at once, plus the numpy stages the
+ * reference runs between those kernels (budget.py, scoring.py, bench.py).
+ *
+ * Data layout (row-major, contiguous, bf16 = IEEE bfloat16):
+ *   window queries  q_win [B, L, Hq, w, d]     the w scoring rows of each head
+ *   keys / values   [B, L, Hkv, T, d]          T >= n_keys (+ decode rows)
+ *   slot s = (b*L + l)*Hkv + kv ; head h = kv*G + g, G = Hq/Hkv
+ *   window row r of slot s = g*w + i  (i = position in the window)
+ */
+#ifndef VLC_H
+#define VLC_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VLC_API __attribute__((visibility("default")))
+#else
+#define VLC_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VLC_OK 0
+#define VLC_EINVAL (-1)       /* argument contract violated  -> ValidationError   */
+#define VLC_EUNSUPPORTED (-2) /* shape outside this build     -> ValidationError   */
+#define VLC_ECUDA (-3)        /* CUDA launch/runtime failure  -> KernelError        */
+
+VLC_API int vlc_abi_version(void);
+VLC_API const char *vlc_strerror(int code);
+VLC_API const char *vlc_last_error(void);
+
+/* float32 t* = smallest x with (double)expf(x) >= p (host libm expf): the
+ * below-threshold test "(double)expf(l - max) < p" of reference
+ * _core.pyx:201-204 is exactly "l - max < t*". */
+VLC_API float vlc_threshold_logit(double p);
+
+/* Rows of col_partial per slot for a window of `rows` = G*w rows. */
+VLC_API int64_t vlc_score_row_blocks(int64_t rows);
+
+/*
+ * K1 score_stats.  Replaces _kernels.stats_tiled (reference _core.pyx:210-242)
+ * for all G heads of every slot: causal logits q.k/sqrt(d) of window row
+ * (absolute index q_base + i) against keys [0, min(n_keys, q_base+i+1)).
+ *   row_max, row_sum : f32 [slots*G*w]       (_core.pyx:142-155)
+ *   col_partial      : f32 [slots, nrb, n_keys] column mass of each 128-row
+ *                      block; per-head col_score when G == 1 and nrb == 1
+ *   below_head       : u64 [slots*G]  entries with exp(l - max) < p, per head
+ *   below_col        : i32 [slots, n_keys] or NULL (per-column counts)
+ * scale <= 0 selects 1/sqrt(head_dim) (zero-padded operands pass the true d's).
+ * Requires n_keys >= q_base + window, head_dim % 16 == 0, head_dim <= 128.
+ */
+VLC_API int vlc_score_stats(const void *q_win, const void *keys, int32_t slots, int32_t group,
+                    int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
+                    int64_t q_base, double p, double scale, float *row_max, float *row_sum,
+                    float *col_partial, uint64_t *below_head, int32_t *below_col,
+                    void *stream);
+
+/*
+ * K2 allocate.  gamma[b,l,h] = below/causal (reference sparsity.py:79),
+ * gamma_mean = mean over heads (sparsity.py:41-43), then
+ * allocate_sparsity_aware (budget.py:86-111): bit-identical to numpy given
+ * equal counts.  Also the ragged offsets of kept sets (kept_off) and cache
+ * segments of kept + cache_extra rows (cache_off), both [B*L*Hkv + 1].
+ * status[b] = 1 when every layer of prompt b is fully sparse (Z == 0,
+ * budget.py:108-109 -> DegenerateSparsityError).
+ */
+VLC_API int vlc_allocate(const uint64_t *below_head, int32_t batch, int32_t layers, int32_t q_heads,
+                 int32_t kv_heads, int64_t window, int64_t n_keys, int64_t q_base,
+                 int64_t prompt_len, double alpha, double beta_min, double beta_max,
+                 int64_t cache_extra, double *gamma, double *gamma_mean, double *beta_pre,
+                 double *beta, int64_t *kept_counts, int64_t *kept_off, int64_t *cache_off,
+                 int32_t *status, void *stream);
+
+/* K2 from a given gamma_mean [B, L] (reference budget.allocate_sparsity_aware
+ * called directly on measured sparsity, budget.py:86-111). */
+VLC_API int vlc_allocate_from_gamma(const double *gamma_mean, int32_t batch, int32_t layers,
+                 int32_t kv_heads, int64_t prompt_len, double alpha, double beta_min,
+                 double beta_max, int64_t cache_extra, double *beta_pre, double *beta,
+                 int64_t *kept_counts, int64_t *kept_off, int64_t *cache_off, int32_t *status,
+                 void *stream);
+
+/*
+ * K3 select.  score = (sum of the slot's column mass) / G (reference
+ * scoring.py:185-201) -- or, when scores_in (f64 [slots, n_keys]) is given,
+ * those scores; then evict (scoring.py:213-235): the last
+ * min(ceil(recent_frac*k), k) positions plus the top of the rest by score,
+ * ties toward the larger index (scoring.py:204-210).  k of slot s is
+ * kept_counts[s / kv_heads].  Writes ascending indices into
+ * kept_idx[kept_off[s] ...] and the owning slot into kept_slot.
+ * scores_out (f64 [slots, n_keys]) may be NULL; key_scratch (u64
+ * [slots, n_keys]) is required only when n_keys > 24576.
+ */
+VLC_API int vlc_select(const float *col_partial, const double *scores_in, int32_t slots,
+               int32_t kv_heads, int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+               const int64_t *kept_counts, const int64_t *kept_off, double recent_frac,
+               int32_t *kept_idx, int32_t *kept_slot, double *scores_out, uint64_t *key_scratch,
+               void *stream);
+
+/*
+ * K4 gather.  Copies keys/values[s, kept_idx] into the cache segment of slot s
+ * (reference bench.py:331-353).  max_rows: host upper bound on sum of kept
+ * counts (sizes the grid; the device total is kept_off[slots]).
+ */
+VLC_API int vlc_gather(const void *keys, const void *values, int32_t slots, int32_t head_dim,
+               int64_t key_rows, const int32_t *kept_idx, const int32_t *kept_slot,
+               const int64_t *kept_off, const int64_t *cache_off, int64_t max_rows,
+               void *k_cache, void *v_cache, void *stream);
+
+/*
+ * K5 decode step `step` (0-based).  Appends k_new/v_new of every slot at row
+ * base_len[b,l] + step of its segment, then out[b,l,h] = softmax(q.K^T/sqrt(d)) V
+ * over the first base_len + step + 1 rows (reference bench.py:362-372 +
+ * _core.pyx:245-278).  q head (b,l,h) is at q + ((b*L+l)*Hq+h)*q_stride,
+ * slot s's new row at k_new/v_new + s*kv_stride (elements).  out: f32
+ * [B*L*Hq, head_dim].  head_dim in {64, 128}, G <= 8; scale as in K1.
+ */
+VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, const void *v_new,
+                    int64_t kv_stride, void *k_cache, void *v_cache, const int64_t *cache_off,
+                    const int64_t *base_len, int64_t step, int32_t batch, int32_t layers,
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float *out,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VLC_H */

@@ -1,0 +1,99 @@
+"""Drop-in for the reference's kernel seam ``vlcache._kernels``.
+
+reference pkg/src/vlcache/_kernels/__init__.py:10-27 exports BACKEND,
+stats_tiled and decode_step with numpy-in/numpy-out semantics.  Here both run
+on the B200 through the C-ABI (K1 with one slot, K5 with one slot); there is
+no CPU fallback -- without the extension or a GPU every call raises
+KernelError.  Inputs are rounded to bf16 on upload (see _device.py).  One
+launch per call makes this seam launch-bound by design; the batched path is
+engine.VLCache.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+from ._device import causal_per_column, to_device_bf16
+from .errors import ValidationError
+
+BACKEND = "b200"
+
+
+def _padded(a: np.ndarray, width: int) -> np.ndarray:
+    if a.shape[1] == width:
+        return a
+    out = np.zeros((a.shape[0], width), dtype=np.float32)
+    out[:, : a.shape[1]] = a
+    return out
+
+
+def stats_tiled(q, keys, q_base, p, tile):
+    """Contract of reference _core.stats_tiled (_core.pyx:210-242):
+    (row_max f32[w], row_sum f64[w], col_score f64[n], below i64[n], causal i64[n]).
+    ``tile`` is the reference's CPU schedule knob; the GPU tiling is fixed."""
+    torch = _lib.require_cuda()
+    q = np.asarray(q, dtype=np.float32)
+    keys = np.asarray(keys, dtype=np.float32)
+    w, d = q.shape
+    n = keys.shape[0]
+    if tile < 1:
+        raise ValidationError(f"tile: must be >= 1, got {tile}")
+    if n < q_base + w:
+        raise ValidationError(f"keys: need n >= q_base + w ({q_base + w}), got {n}")
+    if d > 128:
+        raise ValidationError(f"head_dim: {d} > 128 is not supported")
+    dp = max(16, -(-d // 16) * 16)
+    qd = to_device_bf16(_padded(q, dp))
+    kd = to_device_bf16(_padded(keys, dp))
+    nrb = int(_lib.load().vlc_score_row_blocks(w))
+    f32 = dict(dtype=torch.float32, device="cuda")
+    row_max = torch.empty(w, **f32)
+    row_sum = torch.empty(w, **f32)
+    col = torch.empty(nrb * n, **f32)
+    below_head = torch.zeros(1, dtype=torch.int64, device="cuda")
+    below_col = torch.zeros(n, dtype=torch.int32, device="cuda")
+    # p == 1 is accepted by the reference kernel (test_kernels.py:271-277):
+    # "below 1.0" equals "below the largest double under 1.0" for float exps
+    p_eff = min(float(p), math.nextafter(1.0, 0.0))
+    _lib.call("vlc_score_stats", qd.data_ptr(), kd.data_ptr(), 1, 1, dp, n, n, w, int(q_base), p_eff,
+              1.0 / math.sqrt(d), row_max.data_ptr(), row_sum.data_ptr(), col.data_ptr(),
+              below_head.data_ptr(), below_col.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    col_score = col.view(nrb, n).double().sum(0)
+    return (row_max.cpu().numpy(), row_sum.double().cpu().numpy(), col_score.cpu().numpy(),
+            below_col.long().cpu().numpy(), causal_per_column(n, int(q_base), w))
+
+
+def decode_step(q, keys, values):
+    """Contract of reference _core.decode_step (_core.pyx:245-278): one decode
+    attention pass, q [G, d] against keys/values [n, d] -> f32 [G, d]."""
+    torch = _lib.require_cuda()
+    q = np.asarray(q, dtype=np.float32)
+    keys = np.asarray(keys, dtype=np.float32)
+    values = np.asarray(values, dtype=np.float32)
+    g, d = q.shape
+    n = keys.shape[0]
+    if n < 1:
+        raise ValidationError("keys: need at least one row")
+    if d > 128:
+        raise ValidationError(f"head_dim: {d} > 128 is not supported")
+    if g > 8:  # the kernel serves up to 8 query heads per KV head
+        return np.concatenate([decode_step(q[i:i + 8], keys, values) for i in range(0, g, 8)])
+    dp = 64 if d <= 64 else 128
+    qd = to_device_bf16(_padded(q, dp))
+    kd = to_device_bf16(_padded(keys, dp))
+    vd = to_device_bf16(_padded(values, dp))
+    # one slot: rows [0, n-1) pre-filled, row n-1 appended by the step itself
+    kc, vc = kd.clone(), vd.clone()
+    cache_off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+    base_len = torch.tensor([n - 1], dtype=torch.int64, device="cuda")
+    out = torch.empty((g, dp), dtype=torch.float32, device="cuda")
+    _lib.call("vlc_decode_step", qd.data_ptr(), dp, kd[n - 1:].data_ptr(), vd[n - 1:].data_ptr(), dp,
+              kc.data_ptr(), vc.data_ptr(), cache_off.data_ptr(), base_len.data_ptr(), 0, 1, 1, 1, g,
+              dp, 1.0 / math.sqrt(d), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    return out[:, :d].cpu().numpy()
+
+
+__all__ = ["BACKEND", "stats_tiled", "decode_step"]

@@ -1,0 +1,184 @@
+// select.cu -- K3: per-(b, l, kv) eviction = recent reserve + top-k by score.
+//
+// reference: scoring.py:185-201 (score = sum over the query-head group / G),
+//            scoring.py:213-235 (reserve = min(ceil(frac*k), k); recent
+//            positions [m-reserve, m) kept unconditionally; the rest by
+//            top_k_indices over scores[:m-reserve]),
+//            scoring.py:204-210 (lexsort: descending score, ties toward the
+//            larger index; output ascending).
+// One CTA per slot.  Each float64 score maps to an order-preserving uint64
+// key (sign-flip trick; -0.0 folded onto +0.0 so equal values tie as numpy
+// sees them); an MSB-first 8-bit radix select finds the exact k-th key T;
+// ties at T are resolved toward larger indices by a right-to-left rank; a
+// block scan compacts the kept flags in index order.
+#include "vlc_common.cuh"
+#include "vlc_kernels.h"
+
+namespace vlc {
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int64_t kSmemKeysMax = 24 * 1024;   // scores kept in shared memory up to this many
+
+__device__ __forceinline__ unsigned long long order_key(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 == +0.0
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
+    extern __shared__ unsigned long long keys_smem[];
+    __shared__ unsigned int hist[256];
+    __shared__ long long scan_scratch[32];
+    __shared__ unsigned long long s_prefix, s_mask;
+    __shared__ long long s_want;
+    __shared__ unsigned long long s_min, s_max;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int s = blockIdx.x;
+    const int64_t n = a.n;
+    const int64_t k = a.kept_counts[s / a.Hkv];  // same budget for every KV head of a layer
+    const int64_t reserve = imin((int64_t)ceil(a.recent_frac * (double)k), k);
+    const int64_t nk = k - reserve;
+    const int64_t ncand = n - reserve;
+    unsigned long long* keys = (n <= kSmemKeysMax) ? keys_smem : a.key_scratch + (int64_t)s * n;
+
+    // 1. score = (sum over row blocks, fixed order, fp64) / G  (scoring.py:198-201),
+    //    or the caller's float64 scores when scores_in is given (evict API)
+    unsigned long long kmin = ~0ull, kmax = 0ull;
+    const double group = (double)a.G;
+    for (int64_t j = tid; j < n; j += kThreads) {
+        double sc;
+        if (a.scores_in) {
+            sc = a.scores_in[(int64_t)s * n + j];
+        } else {
+            double acc = 0.0;
+            const float* cp = a.col_partial + (int64_t)s * a.nrb * n + j;
+            for (int rb = 0; rb < a.nrb; ++rb) acc = __dadd_rn(acc, (double)cp[(int64_t)rb * n]);
+            sc = __ddiv_rn(acc, group);
+            if (a.scores) a.scores[(int64_t)s * n + j] = sc;
+        }
+        const unsigned long long key = order_key(sc);
+        keys[j] = key;
+        if (j < ncand) { kmin = min(kmin, key); kmax = max(kmax, key); }
+    }
+    __syncthreads();
+    if (tid == 0) { s_min = ~0ull; s_max = 0ull; s_prefix = 0ull; s_mask = 0ull; s_want = nk; }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(kFull, kmin, o));
+        kmax = max(kmax, __shfl_xor_sync(kFull, kmax, o));
+    }
+    if (nk > 0 && lane == 0) {
+        atomicMin(&s_min, kmin);
+        atomicMax(&s_max, kmax);
+    }
+    __syncthreads();
+
+    // 2. radix select of the nk-th largest key among candidates [0, ncand)
+    if (nk > 0) {
+        // bytes above the first differing byte of (min, max) are common: skip them
+        const unsigned long long diff = s_min ^ s_max;
+        int top_pass = diff ? (63 - __clzll(diff)) / 8 : -1;
+        if (tid == 0 && top_pass < 7) {
+            const int keep_bits = (top_pass + 1) * 8;
+            const unsigned long long m = keep_bits >= 64 ? 0ull : (~0ull << keep_bits);
+            s_prefix = s_min & m;
+            s_mask = m;
+        }
+        __syncthreads();
+        for (int pass = top_pass; pass >= 0; --pass) {
+            const int shift = pass * 8;
+            for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+            __syncthreads();
+            const unsigned long long prefix = s_prefix, mask = s_mask;
+            for (int64_t j0 = 0; j0 < ncand; j0 += kThreads) {
+                const int64_t j = j0 + tid;
+                const bool in = j < ncand && ((keys[j] & mask) == prefix);
+                const unsigned dgt = in ? (unsigned)((keys[j] >> shift) & 255u) : 256u;
+                const unsigned peers = __match_any_sync(kFull, dgt);
+                if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
+            }
+            __syncthreads();
+            if (warp == 0) {
+                // lane L covers digits 255-8L .. 248-8L (descending)
+                unsigned c[8];
+                unsigned tot = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) { c[q] = hist[255 - 8 * lane - q]; tot += c[q]; }
+                unsigned incl = tot;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    unsigned y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const unsigned excl = incl - tot;
+                const long long want = s_want;
+                const bool mine = (long long)excl < want && want <= (long long)incl;
+                if (mine) {
+                    long long cum = excl;
+                    int sel = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (cum + c[q] >= want) { sel = 255 - 8 * lane - q; break; }
+                        cum += c[q];
+                    }
+                    s_want = want - cum;
+                    s_prefix = prefix | ((unsigned long long)sel << shift);
+                    s_mask = mask | (255ull << shift);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const unsigned long long T = s_prefix;
+    const long long need = s_want;   // ties at T to keep (largest indices first)
+
+    // 3. chunked flags in index order.  A tie at T is kept iff fewer than
+    //    `need` ties lie strictly to its right (ties toward the larger index).
+    const int64_t chunk = (n + kThreads - 1) / kThreads;
+    const int64_t c0 = imin(n, (int64_t)tid * chunk), c1 = imin(n, c0 + chunk);
+    long long ties = 0;
+    if (nk > 0)
+        for (int64_t j = c0; j < c1 && j < ncand; ++j) ties += (keys[j] == T);
+    const long long ties_incl = block_inclusive_scan<long long>(ties, scan_scratch);
+    __shared__ long long s_ties_total;
+    if (tid == kThreads - 1) s_ties_total = ties_incl;
+    __syncthreads();
+    const long long ties_from_c0 = s_ties_total - ties_incl + ties;   // ties with index >= c0
+    auto walk = [&](bool write, int64_t out_pos) -> long long {
+        long long right = ties_from_c0, kept = 0;
+        for (int64_t j = c0; j < c1; ++j) {
+            bool keep;
+            if (j >= ncand) keep = true;
+            else if (nk == 0) keep = false;
+            else if (keys[j] > T) keep = true;
+            else if (keys[j] == T) { --right; keep = right < need; }
+            else keep = false;
+            if (keep) {
+                if (write) {
+                    a.kept_idx[out_pos + kept] = (int32_t)j;
+                    a.kept_slot[out_pos + kept] = s;
+                }
+                ++kept;
+            }
+        }
+        return kept;
+    };
+    const long long kept_here = walk(false, 0);
+    const long long pos_incl = block_inclusive_scan<long long>(kept_here, scan_scratch);
+    walk(true, a.kept_off[s] + (pos_incl - kept_here));
+}
+
+}  // namespace
+
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
+    if (a.n > kSmemKeysMax && !a.key_scratch) return cudaErrorInvalidValue;  // needs global scratch
+    const size_t sm = a.n <= kSmemKeysMax ? sizeof(unsigned long long) * (size_t)a.n : 0;
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemKeysMax * 8));
+    select_kernel<<<a.slots, kThreads, sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace vlc

@@ -1,0 +1,218 @@
+// vlc_api.cu -- extern "C" boundary (include/vlc.h): argument contracts,
+// error codes, and dispatch to the sm_100a kernels.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "../../include/vlc.h"
+#include "vlc_kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return VLC_OK;
+    return fail(VLC_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+float threshold_logit(double p) {
+    // walk the float grid around log(p) with the host libm expf -- the same
+    // function the reference's compiled kernel calls (_core.pyx:201)
+    float x = (float)std::log(p);
+    while ((double)expf(x) >= p) x = std::nextafterf(x, -INFINITY);
+    while ((double)expf(x) < p) x = std::nextafterf(x, INFINITY);
+    return x;
+}
+
+float cached_threshold(double p) {
+    static std::mutex mu;
+    static std::unordered_map<double, float> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(p);
+    if (it != cache.end()) return it->second;
+    const float t = threshold_logit(p);
+    cache.emplace(p, t);
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+int vlc_abi_version(void) { return 1; }
+
+const char* vlc_strerror(int code) {
+    switch (code) {
+        case VLC_OK: return "ok";
+        case VLC_EINVAL: return "invalid argument";
+        case VLC_EUNSUPPORTED: return "unsupported shape";
+        case VLC_ECUDA: return "CUDA error";
+        default: return "unknown error";
+    }
+}
+
+const char* vlc_last_error(void) { return g_err; }
+
+float vlc_threshold_logit(double p) { return threshold_logit(p); }
+
+int64_t vlc_score_row_blocks(int64_t rows) { return vlc::score_row_blocks(rows); }
+
+int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t group,
+                    int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
+                    int64_t q_base, double p, double scale, float* row_max, float* row_sum, float* col_partial,
+                    uint64_t* below_head, int32_t* below_col, void* stream) {
+    if (!q_win || !keys || !row_max || !row_sum || !col_partial || !below_head)
+        return fail(VLC_EINVAL, "score_stats: null pointer");
+    if (slots < 1 || group < 1 || window < 1 || n_keys < 1 || q_base < 0)
+        return fail(VLC_EINVAL, "score_stats: need slots, group, window, n_keys >= 1 and q_base >= 0");
+    if (!(p > 0.0 && p < 1.0)) return fail(VLC_EINVAL, "p: must be in (0, 1), got %g", p);
+    if (n_keys < q_base + window)
+        return fail(VLC_EINVAL, "score_stats: n_keys %lld < q_base + window %lld",
+                    (long long)n_keys, (long long)(q_base + window));
+    if (key_rows < n_keys) return fail(VLC_EINVAL, "score_stats: key_rows < n_keys");
+    if (head_dim < 16 || head_dim % 16 || head_dim > 128)
+        return fail(VLC_EUNSUPPORTED, "score_stats: head_dim %d not a multiple of 16 in [16, 128]", head_dim);
+    vlc::ScoreArgs a{};
+    a.q = q_win; a.k = keys; a.slots = slots; a.G = group; a.d = head_dim;
+    a.T = key_rows; a.n = n_keys; a.w = window; a.q_base = q_base;
+    a.inv_scale = (float)(scale > 0.0 ? scale : 1.0 / std::sqrt((double)head_dim));
+    a.t_star = cached_threshold(p);
+    a.row_max = row_max; a.row_sum = row_sum; a.col_partial = col_partial;
+    a.below_head = reinterpret_cast<unsigned long long*>(below_head);
+    a.below_col = below_col;
+    return cuda_status(vlc::launch_score_stats(a, (cudaStream_t)stream), "score_stats");
+}
+
+int vlc_allocate(const uint64_t* below_head, int32_t batch, int32_t layers, int32_t q_heads,
+                 int32_t kv_heads, int64_t window, int64_t n_keys, int64_t q_base,
+                 int64_t prompt_len, double alpha, double beta_min, double beta_max,
+                 int64_t cache_extra, double* gamma, double* gamma_mean, double* beta_pre,
+                 double* beta, int64_t* kept_counts, int64_t* kept_off, int64_t* cache_off,
+                 int32_t* status, void* stream) {
+    if (!below_head || !gamma || !gamma_mean || !beta_pre || !beta || !kept_counts || !kept_off ||
+        !cache_off || !status)
+        return fail(VLC_EINVAL, "allocate: null pointer");
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(VLC_EINVAL, "alpha: must be in (0, 1], got %g", alpha);
+    if (!(beta_min > 0.0 && beta_min <= beta_max))
+        return fail(VLC_EINVAL, "beta_min: need 0 < beta_min <= beta_max");
+    if (prompt_len < 1) return fail(VLC_EINVAL, "prompt_len: must be >= 1, got %lld", (long long)prompt_len);
+    if (batch < 1 || batch > 1024 || layers < 1 || q_heads < 1 || kv_heads < 1 || q_heads % kv_heads)
+        return fail(VLC_EINVAL, "allocate: bad batch/layers/heads");
+    if (window < 1 || n_keys < q_base + window || cache_extra < 0)
+        return fail(VLC_EINVAL, "allocate: bad window");
+    // causal entries of one head's window: sum_i min(n, q_base + i + 1)
+    int64_t causal = 0;
+    for (int64_t i = 0; i < window; ++i) causal += std::min<int64_t>(n_keys, q_base + i + 1);
+    vlc::BudgetArgs a{};
+    a.below_head = reinterpret_cast<const unsigned long long*>(below_head);
+    a.B = batch; a.L = layers; a.Hq = q_heads; a.Hkv = kv_heads;
+    a.causal_per_head = causal; a.prompt_len = prompt_len;
+    a.alpha_times_L = alpha * (double)layers;   // budget.py:110 "alpha * g.size"
+    a.beta_min = beta_min; a.beta_max = beta_max; a.cache_extra = cache_extra;
+    a.gamma = gamma; a.gamma_mean = gamma_mean; a.beta_pre = beta_pre; a.beta = beta;
+    a.kept_counts = kept_counts; a.kept_off = kept_off; a.cache_off = cache_off; a.status = status;
+    return cuda_status(vlc::launch_allocate(a, (cudaStream_t)stream), "allocate");
+}
+
+int vlc_allocate_from_gamma(const double* gamma_mean, int32_t batch, int32_t layers,
+                            int32_t kv_heads, int64_t prompt_len, double alpha, double beta_min,
+                            double beta_max, int64_t cache_extra, double* beta_pre, double* beta,
+                            int64_t* kept_counts, int64_t* kept_off, int64_t* cache_off,
+                            int32_t* status, void* stream) {
+    if (!gamma_mean || !beta_pre || !beta || !kept_counts || !kept_off || !cache_off || !status)
+        return fail(VLC_EINVAL, "allocate: null pointer");
+    if (!(alpha > 0.0 && alpha <= 1.0)) return fail(VLC_EINVAL, "alpha: must be in (0, 1], got %g", alpha);
+    if (!(beta_min > 0.0 && beta_min <= beta_max))
+        return fail(VLC_EINVAL, "beta_min: need 0 < beta_min <= beta_max");
+    if (prompt_len < 1) return fail(VLC_EINVAL, "prompt_len: must be >= 1, got %lld", (long long)prompt_len);
+    if (batch < 1 || batch > 1024 || layers < 1 || kv_heads < 1 || cache_extra < 0)
+        return fail(VLC_EINVAL, "allocate: bad batch/layers/heads");
+    vlc::BudgetArgs a{};
+    a.below_head = nullptr; a.gamma_mean_in = gamma_mean;
+    a.B = batch; a.L = layers; a.Hq = 1; a.Hkv = kv_heads; a.prompt_len = prompt_len;
+    a.alpha_times_L = alpha * (double)layers;
+    a.beta_min = beta_min; a.beta_max = beta_max; a.cache_extra = cache_extra;
+    a.gamma = nullptr; a.gamma_mean = const_cast<double*>(gamma_mean);
+    a.beta_pre = beta_pre; a.beta = beta;
+    a.kept_counts = kept_counts; a.kept_off = kept_off; a.cache_off = cache_off; a.status = status;
+    return cuda_status(vlc::launch_allocate(a, (cudaStream_t)stream), "allocate");
+}
+
+int vlc_select(const float* col_partial, const double* scores_in, int32_t slots, int32_t kv_heads,
+               int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+               const int64_t* kept_counts, const int64_t* kept_off, double recent_frac,
+               int32_t* kept_idx, int32_t* kept_slot, double* scores_out, uint64_t* key_scratch,
+               void* stream) {
+    if ((!col_partial && !scores_in) || !kept_counts || !kept_off || !kept_idx || !kept_slot)
+        return fail(VLC_EINVAL, "select: null pointer");
+    if (slots < 1 || kv_heads < 1 || layers < 1 || group < 1 || n_keys < 1 || window < 1)
+        return fail(VLC_EINVAL, "select: bad shape");
+    if (slots % (kv_heads * layers)) return fail(VLC_EINVAL, "select: slots not a multiple of L*Hkv");
+    if (!(recent_frac >= 0.0 && recent_frac <= 1.0))
+        return fail(VLC_EINVAL, "recent_window_frac: must be in [0, 1], got %g", recent_frac);
+    if (n_keys > (1ll << 31) - 1) return fail(VLC_EUNSUPPORTED, "select: n_keys exceeds int32 indices");
+    if (n_keys > 24 * 1024 && !key_scratch)
+        return fail(VLC_EINVAL, "select: n_keys > 24576 needs key_scratch");
+    vlc::SelectArgs a{};
+    a.col_partial = col_partial; a.slots = slots;
+    a.nrb = (int)vlc::score_row_blocks((int64_t)group * window);
+    a.Hkv = kv_heads; a.L = layers; a.G = group; a.n = n_keys;
+    a.kept_counts = kept_counts; a.kept_off = kept_off; a.recent_frac = recent_frac;
+    a.kept_idx = kept_idx; a.kept_slot = kept_slot; a.scores = scores_out; a.scores_in = scores_in;
+    a.key_scratch = reinterpret_cast<unsigned long long*>(key_scratch);
+    return cuda_status(vlc::launch_select(a, (cudaStream_t)stream), "select");
+}
+
+int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head_dim,
+               int64_t key_rows, const int32_t* kept_idx, const int32_t* kept_slot,
+               const int64_t* kept_off, const int64_t* cache_off, int64_t max_rows,
+               void* k_cache, void* v_cache, void* stream) {
+    if (!keys || !values || !kept_idx || !kept_slot || !kept_off || !cache_off || !k_cache || !v_cache)
+        return fail(VLC_EINVAL, "gather: null pointer");
+    if (slots < 1 || key_rows < 1 || max_rows < 0) return fail(VLC_EINVAL, "gather: bad shape");
+    if (head_dim % 8 || head_dim < 8) return fail(VLC_EUNSUPPORTED, "gather: head_dim %% 8 != 0");
+    vlc::GatherArgs a{};
+    a.k = keys; a.v = values; a.slots = slots; a.d = head_dim; a.T = key_rows;
+    a.kept_idx = kept_idx; a.kept_slot = kept_slot; a.kept_off = kept_off; a.cache_off = cache_off;
+    a.max_rows = max_rows; a.k_cache = k_cache; a.v_cache = v_cache;
+    return cuda_status(vlc::launch_gather(a, (cudaStream_t)stream), "gather");
+}
+
+int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const void* v_new,
+                    int64_t kv_stride, void* k_cache, void* v_cache, const int64_t* cache_off,
+                    const int64_t* base_len, int64_t step, int32_t batch, int32_t layers,
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float* out,
+                    void* stream) {
+    if (!q || !k_new || !v_new || !k_cache || !v_cache || !cache_off || !base_len || !out)
+        return fail(VLC_EINVAL, "decode_step: null pointer");
+    if (batch < 1 || layers < 1 || kv_heads < 1 || group < 1 || step < 0)
+        return fail(VLC_EINVAL, "decode_step: bad shape");
+    if (group > 8) return fail(VLC_EUNSUPPORTED, "decode_step: group size %d > 8", group);
+    if (head_dim != 64 && head_dim != 128)
+        return fail(VLC_EUNSUPPORTED, "decode_step: head_dim %d not in {64, 128}", head_dim);
+    if (q_stride % 8 || kv_stride % 8) return fail(VLC_EINVAL, "decode_step: strides must be 16-byte multiples");
+    vlc::DecodeArgs a{};
+    a.q = q; a.q_stride = q_stride; a.k_new = k_new; a.v_new = v_new; a.kv_stride = kv_stride;
+    a.k_cache = k_cache; a.v_cache = v_cache; a.cache_off = cache_off; a.base_len = base_len;
+    a.step = step; a.slots = batch * layers * kv_heads; a.Hkv = kv_heads; a.L = layers; a.G = group;
+    a.d = head_dim; a.out = out;
+    // reference _core.pyx:257: inv = <float>(1.0 / sqrt(<double> d))
+    a.inv_scale = (float)(scale > 0.0 ? scale : 1.0 / std::sqrt((double)head_dim));
+    return cuda_status(vlc::launch_decode(a, (cudaStream_t)stream), "decode_step");
+}
+
+}  // extern "C"

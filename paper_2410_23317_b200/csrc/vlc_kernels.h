@@ -1,0 +1,98 @@
+// vlc_kernels.h -- internal launcher interface between the C-ABI (vlc_api.cu)
+// and the sm_100a kernels.  Not part of the public boundary (see include/vlc.h).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vlc {
+
+// K1: post-vision attention statistics for every (b, l, kv) slot.
+// Slot s = (b*L + l)*Hkv + kv owns window rows [s*R, s*R + R), R = G*w, i.e.
+// heads kv*G .. kv*G+G-1 of the [B, L, Hq, w, d] window tensor.
+struct ScoreArgs {
+    const void* q;          // bf16 [B*L*Hq, w, d]   (window query rows)
+    const void* k;          // bf16 [B*L*Hkv, T, d]  (keys; rows >= n never read)
+    int slots, G, d;
+    int64_t T, n, w, q_base;
+    float inv_scale, t_star;
+    float* row_max;                    // [slots*R]
+    float* row_sum;                    // [slots*R]
+    float* col_partial;                // [slots, nrb, n]  per row-block column sums
+    unsigned long long* below_head;    // [slots*G]  (zeroed by the launcher)
+    int* below_col;                    // optional [slots, n] (zeroed by the launcher)
+};
+int score_row_blocks(int64_t rows);  // nrb for R rows
+cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st);
+
+// K2: numpy-exact gamma -> gamma' -> beta -> kept counts, plus ragged offsets.
+struct BudgetArgs {
+    const unsigned long long* below_head;  // [B, L, Hq]  (NULL: gamma_mean_in given)
+    const double* gamma_mean_in;           // [B, L]  used when below_head is NULL
+    int B, L, Hq, Hkv;
+    int64_t causal_per_head;   // sum of causal entries of one head's window
+    int64_t prompt_len;        // m (kept counts clip to [1, m])
+    double alpha_times_L, beta_min, beta_max;
+    int64_t cache_extra;       // headroom rows per cache segment (decode appends)
+    double* gamma;             // [B, L, Hq]
+    double* gamma_mean;        // [B, L]
+    double* beta_pre;          // [B, L]
+    double* beta;              // [B, L]
+    int64_t* kept_counts;      // [B, L]
+    int64_t* kept_off;         // [B*L*Hkv + 1]  prefix of kept counts per slot
+    int64_t* cache_off;        // [B*L*Hkv + 1]  prefix of (kept + cache_extra)
+    int* status;               // [B]  0 ok, 1 degenerate (Z == 0)
+};
+cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st);
+
+// K3: per-slot top-k with recent reserve -> ascending kept indices.
+struct SelectArgs {
+    const float* col_partial;  // [slots, nrb, n]
+    int slots, nrb, Hkv, L, G;
+    int64_t n;                 // prompt_len m
+    const int64_t* kept_counts;  // [B, L]
+    const int64_t* kept_off;     // [slots + 1]
+    double recent_frac;
+    int32_t* kept_idx;         // [sum k]
+    int32_t* kept_slot;        // [sum k]  slot of each kept row
+    double* scores;            // optional out [slots, n]
+    const double* scores_in;   // optional in [slots, n]: rank these instead of col_partial
+    unsigned long long* key_scratch;  // [slots, n] when n > 24576
+};
+cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
+
+// K4: compact kept K/V rows into ragged per-slot cache segments.
+struct GatherArgs {
+    const void* k;             // bf16 [slots, T, d]
+    const void* v;             // bf16 [slots, T, d]
+    int slots, d;
+    int64_t T;
+    const int32_t* kept_idx;   // [sum k]
+    const int32_t* kept_slot;  // [sum k]
+    const int64_t* kept_off;   // [slots + 1]
+    const int64_t* cache_off;  // [slots + 1]
+    int64_t max_rows;          // host upper bound on sum k (grid sizing)
+    void* k_cache;             // bf16 [cache rows, d]
+    void* v_cache;
+};
+cudaError_t launch_gather(const GatherArgs& a, cudaStream_t st);
+
+// K5: one decode step over the ragged compressed cache (append + attend).
+struct DecodeArgs {
+    const void* q;             // bf16, head (b,l,h) at q + idx*q_stride
+    int64_t q_stride;          // elements between consecutive (b,l,h) heads
+    const void* k_new;         // bf16, slot s at k_new + s*kv_stride
+    const void* v_new;
+    int64_t kv_stride;
+    void* k_cache;
+    void* v_cache;
+    const int64_t* cache_off;  // [slots + 1]
+    const int64_t* base_len;   // [B, L] rows present before step 0 (kept counts)
+    int64_t step;              // rows appended so far = step
+    int slots, Hkv, L, G, d;
+    float inv_scale;
+    float* out;                // f32 [B*L*Hq, d]
+};
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
+
+}  // namespace vlc

@@ -1,0 +1,288 @@
+"""Batched device API: compress a prefill KV cache, then decode over it.
+
+This is the B200 hot path behind the reference-shaped API (attention.py,
+sparsity.py, budget.py, scoring.py of this package): one C-ABI call per stage
+for every (batch, layer, KV head) slot at once, all enqueued on the current
+torch stream, no host synchronisation between stages.
+
+  K1 score_stats  post-vision Q.K^T statistics        reference _core.pyx:110-242
+  K2 allocate     gamma -> gamma' -> beta -> k_l       budget.py:86-111, sparsity.py:79
+  K3 select       recent reserve + top-k per slot      scoring.py:185-235
+  K4 gather       kept K/V rows -> ragged cache        bench.py:331-353
+  K5 decode_step  append + attend over ragged cache    bench.py:356-372, _core.pyx:245-278
+
+Tensors (bf16, CUDA, contiguous):
+  q_win  [B, L, Hq, w, d]   the w scoring rows (the last w prompt rows)
+  keys   [B, L, Hkv, T, d]  T >= m; rows m.. are the decode steps' new keys
+  values [B, L, Hkv, T, d]
+  q_dec  [B, L, Hq, n, d]   decode-step queries
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from . import _lib
+from .errors import DegenerateSparsityError, ValidationError
+
+_ROW_BLOCK = 128  # K1 rows per CTA; col_partial has ceil(G*w/128) blocks per slot
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    import torch
+
+    return torch.cuda.current_stream().cuda_stream
+
+
+def kept_rows_bound(batch, layers, kv_heads, prompt_len, alpha, beta_min):
+    """Upper bound on sum of kept rows: k_l <= beta_l*m + 1 and
+    sum_l beta_l <= alpha*L + L*beta_min (clip raises a layer by <= beta_min)."""
+    per = min(layers * prompt_len, math.ceil(prompt_len * layers * (alpha + beta_min)) + 2 * layers)
+    return batch * kv_heads * per
+
+
+@dataclass
+class Shape:
+    B: int
+    L: int
+    Hq: int
+    Hkv: int
+    d: int
+    m: int          # prompt length (keys visible to the window)
+    w: int          # scoring window rows (tau, or min(tau, stats_window))
+
+    def __post_init__(self):
+        for k in ("B", "L", "Hq", "Hkv", "d", "m", "w"):
+            if getattr(self, k) < 1:
+                raise ValidationError(f"{k}: must be >= 1, got {getattr(self, k)}")
+        if self.Hq % self.Hkv:
+            raise ValidationError("num_kv_heads: must divide num_query_heads")
+        if self.w > self.m:
+            raise ValidationError(f"window: {self.w} rows exceed prompt_len {self.m}")
+
+    @property
+    def G(self) -> int:
+        return self.Hq // self.Hkv
+
+    @property
+    def slots(self) -> int:
+        return self.B * self.L * self.Hkv
+
+    @property
+    def nrb(self) -> int:
+        return (self.G * self.w + _ROW_BLOCK - 1) // _ROW_BLOCK
+
+    @property
+    def causal_per_head(self) -> int:
+        q_base = self.m - self.w
+        return self.w * (q_base + 1) + self.w * (self.w - 1) // 2
+
+
+class VLCache:
+    """Owns every device buffer of the path for one shape, so repeated calls
+    (and CUDA-graph replays) reuse memory.
+
+    compress(q_win, keys, values) enqueues K1..K4; decode_step / decode
+    enqueue K5.  Results stay on the device; ``check()`` synchronises and
+    raises DegenerateSparsityError like reference budget.py:108-109.
+    """
+
+    def __init__(self, shape: Shape, *, alpha=0.1, p=0.01, recent_frac=0.10, beta_min=0.01,
+                 beta_max=1.0, decode_steps=0, keep_scores=False, device=None, head_shard=None,
+                 scale=None):
+        torch = _lib.require_cuda()
+        if not 0.0 < alpha <= 1.0:
+            raise ValidationError(f"alpha: must be in (0, 1], got {alpha}")
+        if not 0.0 < p < 1.0:
+            raise ValidationError(f"p: must be in (0, 1), got {p}")
+        if not 0.0 <= recent_frac <= 1.0:
+            raise ValidationError(f"recent_window_frac: must be in [0, 1], got {recent_frac}")
+        if not 0.0 < beta_min <= beta_max:
+            raise ValidationError("beta_min: need 0 < beta_min <= beta_max")
+        self.shape = s = shape
+        self.alpha, self.p, self.recent_frac = float(alpha), float(p), float(recent_frac)
+        self.beta_min, self.beta_max = float(beta_min), float(beta_max)
+        self.decode_steps = int(decode_steps)
+        # softmax scale; None -> 1/sqrt(d) (pass the true d's when d is zero-padded)
+        self.scale = 0.0 if scale is None else float(scale)
+        dev = torch.device(device or "cuda")
+        f32, f64, i64, i32 = torch.float32, torch.float64, torch.int64, torch.int32
+        R = s.G * s.w
+        self.row_max = torch.empty(s.slots * R, dtype=f32, device=dev)
+        self.row_sum = torch.empty(s.slots * R, dtype=f32, device=dev)
+        self.col_partial = torch.empty(s.slots * s.nrb * s.m, dtype=f32, device=dev)
+        self.below_head = torch.zeros(s.B * s.L * s.Hq, dtype=i64, device=dev)
+        # KV-head sharding (parallel.py): K2 sees the counts of every head
+        self.head_shard = head_shard
+        if head_shard is not None and (head_shard.kv_per_rank != s.Hkv or head_shard.group_size != s.G):
+            raise ValidationError("head_shard: local shape does not match the shard")
+        self.hq_alloc = head_shard.num_query_heads if head_shard is not None else s.Hq
+        self.below_alloc = self.below_head
+        self.gamma = torch.empty(s.B * s.L * self.hq_alloc, dtype=f64, device=dev)
+        self.gamma_mean = torch.empty(s.B * s.L, dtype=f64, device=dev)
+        self.beta_pre = torch.empty(s.B * s.L, dtype=f64, device=dev)
+        self.beta = torch.empty(s.B * s.L, dtype=f64, device=dev)
+        self.kept_counts = torch.empty(s.B * s.L, dtype=i64, device=dev)
+        self.kept_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
+        self.cache_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
+        self.status = torch.zeros(s.B, dtype=i32, device=dev)
+        self.max_rows = kept_rows_bound(s.B, s.L, s.Hkv, s.m, alpha, beta_min)
+        self.kept_idx = torch.empty(self.max_rows, dtype=i32, device=dev)
+        self.kept_slot = torch.empty(self.max_rows, dtype=i32, device=dev)
+        self.scores = torch.empty(s.slots * s.m, dtype=f64, device=dev) if keep_scores else None
+        self.key_scratch = (torch.empty(s.slots * s.m, dtype=i64, device=dev)
+                            if s.m > 24 * 1024 else None)
+        self.cache_rows = self.max_rows + s.slots * self.decode_steps
+        self.k_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
+        self.v_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
+        self.out = torch.empty(s.B * s.L * s.Hq * s.d, dtype=f32, device=dev)
+        self._graphs = {}
+
+    # ------------------------------------------------------------ stages
+    def _check_inputs(self, q_win, keys, values=None):
+        s = self.shape
+        import torch
+
+        if tuple(q_win.shape) != (s.B, s.L, s.Hq, s.w, s.d):
+            raise ValidationError(f"q_win: expected {(s.B, s.L, s.Hq, s.w, s.d)}, got {tuple(q_win.shape)}")
+        if keys.dim() != 5 or tuple(keys.shape[:3]) != (s.B, s.L, s.Hkv) or keys.shape[4] != s.d \
+                or keys.shape[3] < s.m:
+            raise ValidationError(f"keys: expected [B, L, Hkv, T>=m, d], got {tuple(keys.shape)}")
+        for name, t in (("q_win", q_win), ("keys", keys), ("values", values)):
+            if t is None:
+                continue
+            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+                raise ValidationError(f"{name}: must be a contiguous bf16 CUDA tensor")
+        if values is not None and tuple(values.shape) != tuple(keys.shape):
+            raise ValidationError("values: must match keys")
+
+    def score_stats(self, q_win, keys, below_col=None):
+        """K1 over all slots; fills row_max/row_sum/col_partial/below_head."""
+        s = self.shape
+        self._check_inputs(q_win, keys)
+        _lib.call("vlc_score_stats", q_win.data_ptr(), keys.data_ptr(), s.slots, s.G, s.d,
+                  keys.shape[3], s.m, s.w, s.m - s.w, self.p, self.scale, _ptr(self.row_max), _ptr(self.row_sum),
+                  _ptr(self.col_partial), _ptr(self.below_head), _ptr(below_col), _stream())
+
+    def allocate(self):
+        """K2 from the below-threshold counts currently in below_head."""
+        s = self.shape
+        _lib.call("vlc_allocate", _ptr(self.below_alloc), s.B, s.L, self.hq_alloc, s.Hkv, s.w, s.m, s.m - s.w,
+                  s.m, self.alpha, self.beta_min, self.beta_max, self.decode_steps, _ptr(self.gamma),
+                  _ptr(self.gamma_mean), _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
+                  _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.status), _stream())
+
+    def select(self):
+        s = self.shape
+        _lib.call("vlc_select", _ptr(self.col_partial), 0, s.slots, s.Hkv, s.L, s.G, s.m, s.w,
+                  _ptr(self.kept_counts), _ptr(self.kept_off), self.recent_frac, _ptr(self.kept_idx),
+                  _ptr(self.kept_slot), _ptr(self.scores), _ptr(self.key_scratch), _stream())
+
+    def gather(self, keys, values):
+        s = self.shape
+        self._check_inputs_kv(keys, values)
+        _lib.call("vlc_gather", keys.data_ptr(), values.data_ptr(), s.slots, s.d, keys.shape[3],
+                  _ptr(self.kept_idx), _ptr(self.kept_slot), _ptr(self.kept_off), _ptr(self.cache_off),
+                  self.max_rows, _ptr(self.k_cache), _ptr(self.v_cache), _stream())
+
+    def _check_inputs_kv(self, keys, values):
+        s = self.shape
+        import torch
+
+        for name, t in (("keys", keys), ("values", values)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+                raise ValidationError(f"{name}: must be a contiguous bf16 CUDA tensor")
+            if t.dim() != 5 or tuple(t.shape[:3]) != (s.B, s.L, s.Hkv) or t.shape[4] != s.d:
+                raise ValidationError(f"{name}: expected [B, L, Hkv, T, d], got {tuple(t.shape)}")
+
+    def compress(self, q_win, keys, values=None, group=None):
+        """K1 -> (count exchange across ranks when head-sharded) -> K2 -> K3 -> K4."""
+        self.score_stats(q_win, keys)
+        if self.head_shard is not None:
+            from .parallel import exchange_head_counts
+
+            s = self.shape
+            local = self.below_head.view(s.B, s.L, s.Hq)
+            self.below_alloc = exchange_head_counts(local, self.head_shard, group).reshape(-1)
+        self.allocate()
+        self.select()
+        if values is not None:
+            self.gather(keys, values)
+        return self
+
+    # ------------------------------------------------------------ decode
+    def decode_step(self, q_dec, keys, values, step):
+        """K5 for decode step `step`: appends keys/values row m+step of every
+        slot, attends the G query rows q_dec[..., step, :] of each KV head."""
+        s = self.shape
+        if not 0 <= step < self.decode_steps:
+            raise ValidationError(f"step: must be in [0, {self.decode_steps}), got {step}")
+        n_dec, T = q_dec.shape[3], keys.shape[3]
+        if step >= n_dec or s.m + step >= T:
+            raise ValidationError("step: beyond the provided decode rows")
+        esz = 2
+        _lib.call("vlc_decode_step", q_dec.data_ptr() + step * s.d * esz, n_dec * s.d,
+                  keys.data_ptr() + (s.m + step) * s.d * esz, values.data_ptr() + (s.m + step) * s.d * esz,
+                  T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.cache_off),
+                  _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, _ptr(self.out), _stream())
+        return self.out
+
+    def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None):
+        """n_steps decode steps; with graph=True the launch sequence is captured
+        once into a CUDA graph (per input pointers) and replayed."""
+        import torch
+
+        n = self.decode_steps if n_steps is None else int(n_steps)
+        if outputs is not None or not graph:
+            for t in range(n):
+                self.decode_step(q_dec, keys, values, t)
+                if outputs is not None:
+                    outputs.append(self.out.clone())
+            return self.out
+        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), n)
+        g = self._graphs.get(key)
+        if g is None:
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for t in range(n):   # warm-up launch outside capture
+                    self.decode_step(q_dec, keys, values, t)
+            torch.cuda.current_stream().wait_stream(side)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for t in range(n):
+                    self.decode_step(q_dec, keys, values, t)
+            self._graphs[key] = g
+        g.replay()
+        return self.out
+
+    # ------------------------------------------------------------ results
+    def check(self):
+        """Synchronise and raise like the reference on a degenerate budget."""
+        bad = self.status.nonzero()
+        if bad.numel():
+            raise DegenerateSparsityError(
+                f"every layer is fully sparse; cannot split the budget (batch {bad.flatten().tolist()})")
+
+    def kept_sets(self):
+        """Host copy: kept[b][l][kv] -> int64 numpy array of ascending indices."""
+        s = self.shape
+        self.check()
+        off = self.kept_off.cpu().numpy()
+        idx = self.kept_idx[: int(off[-1])].cpu().numpy().astype("int64")
+        out = []
+        for b in range(s.B):
+            layer_rows = []
+            for l in range(s.L):
+                row = []
+                for kv in range(s.Hkv):
+                    sl = (b * s.L + l) * s.Hkv + kv
+                    row.append(idx[off[sl]:off[sl + 1]])
+                layer_rows.append(row)
+            out.append(layer_rows)
+        return out
