@@ -9,6 +9,7 @@
 // (8 strided accumulators for n <= 128, recursive halving above); the same
 // association is reproduced here with round-to-nearest intrinsics so that no
 // FMA contraction can creep in.  Bit-exact given equal integer counts.
+#include "vlc_common.cuh"
 #include "vlc_kernels.h"
 
 namespace vlc {
@@ -38,58 +39,79 @@ __device__ double pairwise_sum(const double* a, int64_t n, int64_t stride) {
     return __dadd_rn(left, pairwise_sum(a + n2 * stride, n - n2, stride));
 }
 
-// One block, one thread per batch element for the per-batch arithmetic, then a
-// serial prefix over slots by thread 0.
-__global__ void allocate_kernel(BudgetArgs a) {
-    const int b = threadIdx.x;
-    if (b < a.B && !a.below_head) {
-        for (int l = 0; l < a.L; ++l)
-            a.gamma_mean[(int64_t)b * a.L + l] = a.gamma_mean_in[(int64_t)b * a.L + l];
-    }
-    if (b < a.B && a.below_head) {
+// One block.  Phase 1: a thread per (b, l, h) divides the counts; phase 2: a
+// thread per (b, l) takes the numpy-order head mean; phase 3: a thread per b
+// forms Z and the budgets; phase 4: block scan of per-slot sizes -> offsets.
+constexpr int kAllocThreads = 1024;
+
+__global__ void __launch_bounds__(kAllocThreads) allocate_kernel(BudgetArgs a) {
+    __shared__ long long scan_k[32], scan_c[32];
+    const int64_t BL = (int64_t)a.B * a.L;
+    if (a.below_head) {
         const double causal = (double)a.causal_per_head;
-        double* g = a.gamma + (int64_t)b * a.L * a.Hq;
-        for (int l = 0; l < a.L; ++l) {
-            for (int h = 0; h < a.Hq; ++h) {
-                const int64_t idx = ((int64_t)b * a.L + l) * a.Hq + h;
-                g[(int64_t)l * a.Hq + h] = __ddiv_rn((double)a.below_head[idx], causal);
-            }
-            a.gamma_mean[(int64_t)b * a.L + l] =
-                __ddiv_rn(pairwise_sum(g + (int64_t)l * a.Hq, a.Hq, 1), (double)a.Hq);
-        }
-    }
-    if (b < a.B) {
-        double* gm = a.gamma_mean + (int64_t)b * a.L;
-        // 1 - gamma' into beta_pre as scratch, then Z by pairwise sum
-        double* pre = a.beta_pre + (int64_t)b * a.L;
-        for (int l = 0; l < a.L; ++l) pre[l] = __dadd_rn(1.0, -gm[l]);
-        const double z = pairwise_sum(pre, a.L, 1);
-        a.status[b] = (z == 0.0) ? 1 : 0;
-        for (int l = 0; l < a.L; ++l) {
-            const double p = __dmul_rn(__ddiv_rn(pre[l], z), a.alpha_times_L);
-            pre[l] = p;
-            const double be = fmin(fmax(p, a.beta_min), a.beta_max);
-            a.beta[(int64_t)b * a.L + l] = be;
-            double kc = ceil(__dmul_rn(be, (double)a.prompt_len));
-            int64_t k = (z == 0.0) ? 1 : (int64_t)kc;
-            if (k < 1) k = 1;
-            if (k > a.prompt_len) k = a.prompt_len;
-            a.kept_counts[(int64_t)b * a.L + l] = k;
-        }
+        for (int64_t idx = threadIdx.x; idx < BL * a.Hq; idx += blockDim.x)
+            a.gamma[idx] = __ddiv_rn((double)a.below_head[idx], causal);
+        __syncthreads();
+        for (int64_t bl = threadIdx.x; bl < BL; bl += blockDim.x)
+            a.gamma_mean[bl] = __ddiv_rn(pairwise_sum(a.gamma + bl * a.Hq, a.Hq, 1), (double)a.Hq);
+    } else {
+        for (int64_t bl = threadIdx.x; bl < BL; bl += blockDim.x) a.gamma_mean[bl] = a.gamma_mean_in[bl];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t ko = 0, co = 0;
-        const int64_t slots = (int64_t)a.B * a.L * a.Hkv;
-        for (int64_t s = 0; s < slots; ++s) {
-            const int64_t k = a.kept_counts[s / a.Hkv];
-            a.kept_off[s] = ko;
-            a.cache_off[s] = co;
-            ko += k;
-            co += k + a.cache_extra;
-        }
-        a.kept_off[slots] = ko;
-        a.cache_off[slots] = co;
+    // 1 - gamma' into beta_pre as scratch
+    for (int64_t bl = threadIdx.x; bl < BL; bl += blockDim.x) a.beta_pre[bl] = __dadd_rn(1.0, -a.gamma_mean[bl]);
+    __syncthreads();
+    __shared__ double z_s[1024];
+    for (int b = threadIdx.x; b < a.B; b += blockDim.x) {
+        const double z = pairwise_sum(a.beta_pre + (int64_t)b * a.L, a.L, 1);
+        z_s[b] = z;
+        a.status[b] = (z == 0.0) ? 1 : 0;
+    }
+    __syncthreads();
+    for (int64_t bl = threadIdx.x; bl < BL; bl += blockDim.x) {
+        const double z = z_s[bl / a.L];
+        const double p = __dmul_rn(__ddiv_rn(a.beta_pre[bl], z), a.alpha_times_L);
+        const double be = fmin(fmax(p, a.beta_min), a.beta_max);
+        a.beta[bl] = be;
+        const double kc = ceil(__dmul_rn(be, (double)a.prompt_len));
+        int64_t k = (z == 0.0) ? 1 : (int64_t)kc;
+        if (k < 1) k = 1;
+        if (k > a.prompt_len) k = a.prompt_len;
+        a.kept_counts[bl] = k;
+    }
+    __syncthreads();
+    for (int64_t bl = threadIdx.x; bl < BL; bl += blockDim.x) {
+        const double z = z_s[bl / a.L];
+        a.beta_pre[bl] = __dmul_rn(__ddiv_rn(a.beta_pre[bl], z), a.alpha_times_L);
+    }
+    // offsets: chunked exclusive scan over slots (slot s uses kept_counts[s / Hkv])
+    const int64_t slots = BL * a.Hkv;
+    const int64_t chunk = (slots + blockDim.x - 1) / blockDim.x;
+    const int64_t c0 = imin(slots, (int64_t)threadIdx.x * chunk), c1 = imin(slots, c0 + chunk);
+    long long sk = 0, sc = 0, sw = 0;
+    for (int64_t sl = c0; sl < c1; ++sl) {
+        const int64_t k = a.kept_counts[sl / a.Hkv];
+        sk += k;
+        sc += k + a.cache_extra;
+        sw += (k + a.cache_extra + kDecodeChunk - 1) / kDecodeChunk;
+    }
+    const long long ik = block_inclusive_scan<long long>(sk, scan_k);
+    const long long ic = block_inclusive_scan<long long>(sc, scan_c);
+    const long long iw = block_inclusive_scan<long long>(sw, scan_k);
+    long long ok = ik - sk, oc = ic - sc, ow = iw - sw;
+    for (int64_t sl = c0; sl < c1; ++sl) {
+        const int64_t k = a.kept_counts[sl / a.Hkv];
+        a.kept_off[sl] = ok;
+        a.cache_off[sl] = oc;
+        if (a.chunk_off) a.chunk_off[sl] = ow;
+        ok += k;
+        oc += k + a.cache_extra;
+        ow += (k + a.cache_extra + kDecodeChunk - 1) / kDecodeChunk;
+    }
+    if (threadIdx.x == blockDim.x - 1) {
+        a.kept_off[slots] = ik;
+        a.cache_off[slots] = ic;
+        if (a.chunk_off) a.chunk_off[slots] = iw;
     }
 }
 
@@ -97,8 +119,7 @@ __global__ void allocate_kernel(BudgetArgs a) {
 
 cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st) {
     if (a.B > 1024) return cudaErrorInvalidValue;
-    const int threads = ((a.B + 31) / 32) * 32;
-    allocate_kernel<<<1, threads, 0, st>>>(a);
+    allocate_kernel<<<1, kAllocThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

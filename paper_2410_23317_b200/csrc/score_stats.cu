@@ -5,6 +5,8 @@
 // streamed 32 per chunk through shared memory.  Logits come from CUDA-core
 // FMAs in this first version; the softmax/threshold/column epilogue
 // (score_epilogue.cuh) is the one the tcgen05 producer feeds.
+#include <cstdlib>
+
 #include "score_epilogue.cuh"
 #include "vlc_kernels.h"
 
@@ -138,6 +140,13 @@ cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st) {
         e = cudaMemsetAsync(a.below_col, 0, sizeof(int) * a.slots * a.n, st);
         if (e != cudaSuccess) return e;
     }
+    // tcgen05 path (score_stats_tc.cu); the CUDA-core kernel above is kept only
+    // as a debugging cross-check behind VLC_K1_CUDA_CORE=1
+    static const bool cuda_core = [] {
+        const char* v = getenv("VLC_K1_CUDA_CORE");
+        return v && v[0] == '1';
+    }();
+    if (!cuda_core) return launch_score_stats_tc(a, nrb, st);
     dim3 grid(nrb, a.slots);
     if (a.d <= 64) {
         const size_t sm = sizeof(float) * (64 * kRows + kChunk * 64);

@@ -7,6 +7,8 @@
 
 namespace vlc {
 
+constexpr int kDecodeChunk = 64;   // keys per K5 work item
+
 // K1: post-vision attention statistics for every (b, l, kv) slot.
 // Slot s = (b*L + l)*Hkv + kv owns window rows [s*R, s*R + R), R = G*w, i.e.
 // heads kv*G .. kv*G+G-1 of the [B, L, Hq, w, d] window tensor.
@@ -24,6 +26,7 @@ struct ScoreArgs {
 };
 int score_row_blocks(int64_t rows);  // nrb for R rows
 cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st);
+cudaError_t launch_score_stats_tc(const ScoreArgs& a, int nrb, cudaStream_t st);  // head_dim 64 / 128
 
 // K2: numpy-exact gamma -> gamma' -> beta -> kept counts, plus ragged offsets.
 struct BudgetArgs {
@@ -41,6 +44,7 @@ struct BudgetArgs {
     int64_t* kept_counts;      // [B, L]
     int64_t* kept_off;         // [B*L*Hkv + 1]  prefix of kept counts per slot
     int64_t* cache_off;        // [B*L*Hkv + 1]  prefix of (kept + cache_extra)
+    int64_t* chunk_off;        // optional [B*L*Hkv + 1] prefix of K5 work items per slot
     int* status;               // [B]  0 ok, 1 degenerate (Z == 0)
 };
 cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st);
@@ -92,6 +96,10 @@ struct DecodeArgs {
     int slots, Hkv, L, G, d;
     float inv_scale;
     float* out;                // f32 [B*L*Hq, d]
+    const int64_t* chunk_off;  // [slots + 1] work items (kDecodeChunk keys) per slot
+    int* tickets;              // [slots] zero-initialised completion counters
+    float* partials;           // [items, G, d + 2]
+    int64_t max_items;         // host bound on chunk_off[slots] (grid sizing)
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 

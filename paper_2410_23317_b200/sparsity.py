@@ -53,7 +53,11 @@ class LayerSparsity:
 
 
 def padded_head_dim(d: int) -> int:
-    return max(16, -(-d // 16) * 16)
+    """K1 runs 64- or 128-wide tiles; smaller head dims are zero-padded (the
+    softmax scale of the true d is passed explicitly)."""
+    if d > 128:
+        raise ValidationError(f"head_dim: {d} > 128 is not supported")
+    return 64 if d <= 64 else 128
 
 
 def run_window(trace: AttentionTrace, start: int, end: int, p: float, keep_scores: bool = False):
