@@ -76,9 +76,8 @@ VLC_API int vlc_score_stats(const void *q_win, const void *keys, int32_t slots, 
  * K2 allocate.  gamma[b,l,h] = below/causal (reference sparsity.py:79),
  * gamma_mean = mean over heads (sparsity.py:41-43), then
  * allocate_sparsity_aware (budget.py:86-111): bit-identical to numpy given
- * equal counts.  Also the ragged offsets of kept sets (kept_off), of cache
- * segments of kept + cache_extra rows (cache_off) and of K5's work items
- * (chunk_off, may be NULL), all [B*L*Hkv + 1].
+ * equal counts.  Also the ragged offsets of kept sets (kept_off) and of cache
+ * segments of kept + cache_extra rows (cache_off), both [B*L*Hkv + 1].
  * status[b] = 1 when every layer of prompt b is fully sparse (Z == 0,
  * budget.py:108-109 -> DegenerateSparsityError).
  */
@@ -87,15 +86,15 @@ VLC_API int vlc_allocate(const uint64_t *below_head, int32_t batch, int32_t laye
                  int64_t prompt_len, double alpha, double beta_min, double beta_max,
                  int64_t cache_extra, double *gamma, double *gamma_mean, double *beta_pre,
                  double *beta, int64_t *kept_counts, int64_t *kept_off, int64_t *cache_off,
-                 int64_t *chunk_off, int32_t *status, void *stream);
+                 int32_t *status, void *stream);
 
 /* K2 from a given gamma_mean [B, L] (reference budget.allocate_sparsity_aware
  * called directly on measured sparsity, budget.py:86-111). */
 VLC_API int vlc_allocate_from_gamma(const double *gamma_mean, int32_t batch, int32_t layers,
                  int32_t kv_heads, int64_t prompt_len, double alpha, double beta_min,
                  double beta_max, int64_t cache_extra, double *beta_pre, double *beta,
-                 int64_t *kept_counts, int64_t *kept_off, int64_t *cache_off, int64_t *chunk_off,
-                 int32_t *status, void *stream);
+                 int64_t *kept_counts, int64_t *kept_off, int64_t *cache_off, int32_t *status,
+                 void *stream);
 
 /*
  * K3 select.  score = (sum of the slot's column mass) / G (reference
@@ -131,20 +130,14 @@ VLC_API int vlc_gather(const void *keys, const void *values, int32_t slots, int3
  * _core.pyx:245-278).  q head (b,l,h) is at q + ((b*L+l)*Hq+h)*q_stride,
  * slot s's new row at k_new/v_new + s*kv_stride (elements).  out: f32
  * [B*L*Hq, head_dim].  head_dim in {64, 128}, G <= 8; scale as in K1.
- * Split-K work list: chunk_off from vlc_allocate (cache_extra = steps);
- * tickets: i32 [slots] zeroed once before the first step (self-resetting);
- * partials: f32 [max_items * G * (head_dim + 2)], max_items from
- * vlc_decode_max_items.
+ * No workspace: each slot is split across an 8-CTA cluster that merges its
+ * partial softmax states through distributed shared memory.
  */
 VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, const void *v_new,
                     int64_t kv_stride, void *k_cache, void *v_cache, const int64_t *cache_off,
                     const int64_t *base_len, int64_t step, int32_t batch, int32_t layers,
-                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale,
-                    const int64_t *chunk_off, int32_t *tickets, float *partials, int64_t max_items,
-                    float *out, void *stream);
-
-/* Upper bound on K5 work items for a cache of at most max_kept_rows kept rows. */
-VLC_API int64_t vlc_decode_max_items(int64_t max_kept_rows, int64_t slots, int64_t cache_extra);
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float *out,
+                    void *stream);
 
 #ifdef __cplusplus
 }

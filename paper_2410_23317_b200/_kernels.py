@@ -89,15 +89,10 @@ def decode_step(q, keys, values):
     kc, vc = kd.clone(), vd.clone()
     cache_off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
     base_len = torch.tensor([n - 1], dtype=torch.int64, device="cuda")
-    items = int(_lib.load().vlc_decode_max_items(n, 1, 1))
-    chunk_off = torch.tensor([0, -(-n // 64)], dtype=torch.int64, device="cuda")
-    tickets = torch.zeros(1, dtype=torch.int32, device="cuda")
-    partials = torch.empty(items * g * (dp + 2), dtype=torch.float32, device="cuda")
     out = torch.empty((g, dp), dtype=torch.float32, device="cuda")
     _lib.call("vlc_decode_step", qd.data_ptr(), dp, kd[n - 1:].data_ptr(), vd[n - 1:].data_ptr(), dp,
               kc.data_ptr(), vc.data_ptr(), cache_off.data_ptr(), base_len.data_ptr(), 0, 1, 1, 1, g,
-              dp, 1.0 / math.sqrt(d), chunk_off.data_ptr(), tickets.data_ptr(), partials.data_ptr(), items,
-              out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+              dp, 1.0 / math.sqrt(d), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
     return out[:, :d].cpu().numpy()
 
 

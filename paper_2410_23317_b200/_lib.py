@@ -32,15 +32,14 @@ _SIGNATURES = {
     "vlc_score_stats": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64,
                                        _F64, _P, _P, _P, _P, _P, _P]),
     "vlc_allocate": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64, _F64,
-                                    _F64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+                                    _F64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vlc_allocate_from_gamma": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _F64, _F64, _F64, _I64,
-                                               _P, _P, _P, _P, _P, _P, _P, _P]),
+                                               _P, _P, _P, _P, _P, _P, _P]),
     "vlc_select": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I64, _I64, _P, _P, _F64, _P, _P,
                                   _P, _P, _P]),
     "vlc_gather": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
     "vlc_decode_step": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _P, _P, _P, _P, _I64, _I32, _I32,
-                                       _I32, _I32, _I32, _F64, _P, _P, _P, _I64, _P, _P]),
-    "vlc_decode_max_items": (_I64, [_I64, _I64, _I64]),
+                                       _I32, _I32, _I32, _F64, _P, _P]),
 }
 
 _lib = None

@@ -88,30 +88,25 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(BudgetArgs a) {
     const int64_t slots = BL * a.Hkv;
     const int64_t chunk = (slots + blockDim.x - 1) / blockDim.x;
     const int64_t c0 = imin(slots, (int64_t)threadIdx.x * chunk), c1 = imin(slots, c0 + chunk);
-    long long sk = 0, sc = 0, sw = 0;
+    long long sk = 0, sc = 0;
     for (int64_t sl = c0; sl < c1; ++sl) {
         const int64_t k = a.kept_counts[sl / a.Hkv];
         sk += k;
         sc += k + a.cache_extra;
-        sw += (k + a.cache_extra + kDecodeChunk - 1) / kDecodeChunk;
     }
     const long long ik = block_inclusive_scan<long long>(sk, scan_k);
     const long long ic = block_inclusive_scan<long long>(sc, scan_c);
-    const long long iw = block_inclusive_scan<long long>(sw, scan_k);
-    long long ok = ik - sk, oc = ic - sc, ow = iw - sw;
+    long long ok = ik - sk, oc = ic - sc;
     for (int64_t sl = c0; sl < c1; ++sl) {
         const int64_t k = a.kept_counts[sl / a.Hkv];
         a.kept_off[sl] = ok;
         a.cache_off[sl] = oc;
-        if (a.chunk_off) a.chunk_off[sl] = ow;
         ok += k;
         oc += k + a.cache_extra;
-        ow += (k + a.cache_extra + kDecodeChunk - 1) / kDecodeChunk;
     }
     if (threadIdx.x == blockDim.x - 1) {
         a.kept_off[slots] = ik;
         a.cache_off[slots] = ic;
-        if (a.chunk_off) a.chunk_off[slots] = iw;
     }
 }
 

@@ -6,12 +6,17 @@
 // CTA = (slot, block of 128 window rows).  Warp roles (384 threads):
 //   warp 0      TMA producer: the Q block once, then every 128-key tile of the
 //               slot twice (pass 1, pass 2) into a 3-stage swizzled ring
-//   warp 1      MMA issuer: S = Q K^T, M=128 x N=128, K = head_dim, bf16 in,
-//               fp32 accumulate in TMEM (two accumulator stages, 256 columns)
+//   warp 1      MMA issuer, M=128 x N=128, K = head_dim, bf16 in, fp32
+//               accumulate in TMEM (two accumulator stages, 256 columns).
+//               Pass 1 computes Q K^T (rows on TMEM lanes), pass 2 K Q^T
+//               (keys on TMEM lanes) from the same shared-memory operands.
 //   warp 2      TMEM allocator
-//   warps 4-11  epilogue: thread = (window row, half of the tile's columns);
-//               tcgen05.ld 32 columns at a time -> score_epilogue.cuh.
-// The score matrix never leaves the SM: TMEM -> registers -> column sums.
+//   warps 4-11  epilogue, tcgen05.ld 32 columns at a time:
+//               pass 1: thread = window row -> running max / sum (serial);
+//               pass 2: thread = key -> column mass and below-threshold
+//               counts, serial over the block's rows, so neither pass needs a
+//               cross-lane reduction per entry.
+// The score matrix never leaves the SM: TMEM -> registers -> statistics.
 #include <cuda.h>
 
 #include <mutex>
@@ -38,10 +43,20 @@ struct Layout {
     static constexpr uint32_t kQBytes = KB * kQRegion;
     static constexpr uint32_t kKBytes = KB * kKRegion;      // one stage
     static constexpr uint32_t kBarOff = kQBytes + kStages * kKBytes;
-    static constexpr uint32_t kColOff = kBarOff + 256;      // 2 x 4 x 128 floats
-    static constexpr uint32_t kRowOff = kColOff + 2 * 4 * kN * 4;   // 2 x 128 x (m, s)
-    static constexpr uint32_t kBytes = kRowOff + 2 * kM * 8 + 1024; // + alignment slack
+    static constexpr uint32_t kColOff = kBarOff + 256;               // f32 [2 parity][2 half][kN]
+    static constexpr uint32_t kKcntOff = kColOff + 4 * kN * 4;       // i32 [2][2][kN]
+    static constexpr uint32_t kRowOff = kKcntOff + 4 * kN * 4;       // float2 [2 half][kM]
+    static constexpr uint32_t kConstOff = kRowOff + 2 * kM * 8;      // mb, ls, t2 f32 + lim i32, [kM] each
+    static constexpr uint32_t kHcntOff = kConstOff + 4 * kM * 4;     // i32 [kM] head counters
+    static constexpr uint32_t kBytes = kHcntOff + kM * 4 + 1024;     // + alignment slack
 };
+
+VLC_DEV float max32(const float (&l)[32]) {
+    float m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = fmaxf(fmaxf(l[4 * k], l[4 * k + 1]), fmaxf(l[4 * k + 2], l[4 * k + 3]));
+    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -57,8 +72,14 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     uint64_t* tfull = qfull + 1;              // [2]
     uint64_t* tempty = tfull + 2;             // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* colbuf = reinterpret_cast<float*>(smem + LY::kColOff);   // [2][4][kN]
-    float2* rowstat = reinterpret_cast<float2*>(smem + LY::kRowOff); // [2][kM]
+    float* colbuf = reinterpret_cast<float*>(smem + LY::kColOff);
+    int* kcntbuf = reinterpret_cast<int*>(smem + LY::kKcntOff);
+    float2* rowstat = reinterpret_cast<float2*>(smem + LY::kRowOff);
+    float* c_mb = reinterpret_cast<float*>(smem + LY::kConstOff);    // row max (raw dot) * c1
+    float* c_ls = c_mb + kM;                                          // log2(row sum)
+    float* c_t2 = c_ls + kM;                                          // threshold on u (-inf: no row)
+    int* c_lim = reinterpret_cast<int*>(c_t2 + kM);                   // last visible key (-1: no row)
+    int* hcnt = reinterpret_cast<int*>(smem + LY::kHcntOff);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.y, rb = blockIdx.x;
@@ -69,6 +90,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const int64_t blk_end = imin(a.n, a.q_base + i_max + 1);   // keys any row here can see
     const int T = (int)((blk_end + kN - 1) / kN);
     const int iters = 2 * T;
+    const int64_t head0 = r_first / a.w;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) { sm100::mbar_init(full + i, 1); sm100::mbar_init(empty + i, 1); }
@@ -77,6 +99,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         sm100::fence_barrier_init();
         sm100::fence_proxy_async();
     }
+    if (threadIdx.x < kM) hcnt[threadIdx.x] = 0;
     if (warp == 2) sm100::tmem_alloc(tmem_slot, kTmemCols);
     sm100::tc_fence_before();
     __syncthreads();
@@ -103,8 +126,10 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
     } else if (warp == 1 && lane == 0) {
         // ------------------------------------------------ MMA issuer
+        // pass 1: D[row, key] = Q K^T (rows on TMEM lanes); pass 2: D[key, row]
+        // = K Q^T (keys on TMEM lanes) -- same operands, swapped roles
         constexpr uint32_t idesc = sm100::idesc_bf16_f32(kM, kN);
-        const uint32_t q_base_addr = sm100::smem_u32(smem);
+        const uint32_t q_addr = sm100::smem_u32(smem);
         sm100::mbar_wait(qfull, 0);
         for (int it = 0; it < iters; ++it) {
             const int st = it % kStages;
@@ -115,13 +140,15 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::mbar_wait(full + st, ph);
             sm100::tc_fence_after();
             const uint32_t k_addr = sm100::smem_u32(smem + LY::kQBytes + st * LY::kKBytes);
+            const bool rows_on_lanes = it < T;
 #pragma unroll
             for (int kb = 0; kb < LY::KB; ++kb) {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {   // 4 x 16 elements = one 128 B swizzle row
-                    const uint64_t ad = sm100::sdesc_k_sw128(q_base_addr + kb * LY::kQRegion + kk * 32);
-                    const uint64_t bd = sm100::sdesc_k_sw128(k_addr + kb * LY::kKRegion + kk * 32);
-                    sm100::mma_bf16(tmem + acc * kN, ad, bd, idesc, (kb | kk) != 0);
+                    const uint64_t qd = sm100::sdesc_k_sw128(q_addr + kb * LY::kQRegion + kk * 32);
+                    const uint64_t kd = sm100::sdesc_k_sw128(k_addr + kb * LY::kKRegion + kk * 32);
+                    sm100::mma_bf16(tmem + acc * kN, rows_on_lanes ? qd : kd, rows_on_lanes ? kd : qd, idesc,
+                                    (kb | kk) != 0);
                 }
             }
             sm100::mma_commit(empty + st);   // K stage reusable once these MMAs retire
@@ -130,96 +157,154 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int ew = warp - 4, sub = warp & 3, half = ew >> 2;
-        const int row_local = 32 * sub + lane;
-        const int64_t r = r_first + row_local;
-        const bool row_ok = r < R;
-        const int64_t i = row_ok ? r % a.w : 0;
-        const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
+        const int lane_idx = 32 * sub + lane;                  // TMEM lane of this thread
         const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16);
+        const float c1 = a.inv_scale * kLog2e;
         float l[32];
 
-        RowStats st{-INFINITY, 0.f};
-        for (int it = 0; it < T; ++it) {
-            const int acc = it & 1;
-            sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
-            sm100::tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int col0 = half * 64 + c * 32;
-                sm100::tmem_ld32(lane_addr + acc * kN + col0, l);
-#pragma unroll
-                for (int k = 0; k < 32; ++k) l[k] *= a.inv_scale;
-                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + col0)));
-                pass1_chunk(l, valid, st);
-            }
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tempty + acc);
-        }
-        // merge the two column halves of each row (same formula on both sides)
-        rowstat[half * kM + row_local] = make_float2(st.m, st.s);
-        sm100::named_bar_sync(1, kEpiWarps * 32);
+        // ---- pass 1 (thread = window row): running max of raw dots, rescaled sum
         {
-            const float2 h0 = rowstat[row_local], h1 = rowstat[kM + row_local];
-            const float m = fmaxf(h0.x, h1.x);
-            float sum = 0.f;
-            if (h0.x != -INFINITY) sum += h0.y * ex2((h0.x - m) * kLog2e);
-            if (h1.x != -INFINITY) sum += h1.y * ex2((h1.x - m) * kLog2e);
-            st.m = m;
-            st.s = sum;
+            const int64_t r = r_first + lane_idx;
+            const bool row_ok = r < R;
+            const int64_t i = row_ok ? r % a.w : 0;
+            const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
+            float m = -INFINITY, sum = 0.f;
+            for (int it = 0; it < T; ++it) {
+                const int acc = it & 1;
+                sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
+                sm100::tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int col0 = half * 64 + c * 32;
+                    sm100::tmem_ld32(lane_addr + acc * kN + col0, l);
+                    const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + col0)));
+                    const bool full_chunk = __all_sync(kFull, valid == 32);
+                    float cmax;
+                    if (full_chunk) {
+                        cmax = max32(l);
+                    } else {
+                        cmax = -INFINITY;
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+                    }
+                    if (cmax > m) {
+                        sum *= ex2((m - cmax) * c1);   // 0 while m == -inf
+                        m = cmax;
+                    }
+                    const float mb = m * c1;
+                    float acc_s = 0.f;
+                    if (full_chunk) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                    }
+                    sum += acc_s;
+                }
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + acc);
+            }
+            rowstat[half * kM + lane_idx] = make_float2(m, sum);
+            sm100::named_bar_sync(1, kEpiWarps * 32);
+            if (half == 0) {
+                const float2 h0 = rowstat[lane_idx], h1 = rowstat[kM + lane_idx];
+                const float M = fmaxf(h0.x, h1.x);
+                float S = 0.f;
+                if (h0.x != -INFINITY) S += h0.y * ex2((h0.x - M) * c1);
+                if (h1.x != -INFINITY) S += h1.y * ex2((h1.x - M) * c1);
+                if (row_ok) {
+                    a.row_max[(int64_t)s * R + r] = M * a.inv_scale;
+                    a.row_sum[(int64_t)s * R + r] = S;
+                    c_mb[lane_idx] = M * c1;
+                    c_ls[lane_idx] = __log2f(S);
+                    c_t2[lane_idx] = a.t_star * kLog2e;
+                    c_lim[lane_idx] = (int)(a.q_base + i);
+                } else {
+                    c_mb[lane_idx] = INFINITY;    // u = -inf: no mass
+                    c_ls[lane_idx] = 0.f;
+                    c_t2[lane_idx] = -INFINITY;   // never below
+                    c_lim[lane_idx] = -1;         // sees no key
+                }
+            }
+            sm100::named_bar_sync(1, kEpiWarps * 32);
         }
-        const float log2s = row_ok ? __log2f(st.s) : 0.f;
 
-        int below = 0;
+        // ---- pass 2 (thread = key): column mass and below-threshold counts
+        //   u = l*c1 - mb_r ~ log2(exp(logit - max));  below <=> u < t* log2e;
+        //   mass = 2^(u - log2 S_r).  Serial over the CTA's rows: no cross-lane
+        //   reduction, and every key column follows the same summation order.
         float* colp = a.col_partial + ((int64_t)s * nrb + rb) * a.n;
         for (int it = T; it < iters; ++it) {
             const int acc = it & 1;
             const int t = it - T;
             const int p = t & 1;
+            const int j = t * kN + lane_idx;                     // this thread's key
+            const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
             sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
             sm100::tc_fence_after();
+            float colsum = 0.f;
+            int kcnt = 0;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int col0 = half * 64 + c * 32;
-                sm100::tmem_ld32(lane_addr + acc * kN + col0, l);
+                const int r0 = half * 64 + c * 32;
+                sm100::tmem_ld32(lane_addr + acc * kN + r0, l);
+                float csum = 0.f;
+                int cnt = 0;
+                if (all_visible) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) l[k] *= a.inv_scale;
-                const int64_t j0 = (int64_t)t * kN + col0;
-                const int valid = (int)imax(0, imin(32, row_end - j0));
-                float e[32];
-                below += pass2_chunk(l, valid, st.m, log2s, a.t_star, e);
-                colbuf[(p * 4 + sub) * kN + col0 + lane] = transpose_reduce32(e, lane);
-                if (a.below_col) {
-                    int bc[32];
+                    for (int k = 0; k < 32; ++k) {
+                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                        cnt += u < c_t2[r0 + k] ? 1 : 0;
+                        csum += ex2(u - c_ls[r0 + k]);
+                    }
+                } else {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) bc[k] = (k < valid && (l[k] - st.m) < a.t_star) ? 1 : 0;
-                    const int cnt = transpose_reduce32(bc, lane);
-                    if (cnt && j0 + lane < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j0 + lane, cnt);
+                    for (int k = 0; k < 32; ++k) {
+                        const bool vis = j <= c_lim[r0 + k];
+                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                        cnt += (vis && u < c_t2[r0 + k]) ? 1 : 0;
+                        csum += vis ? ex2(u - c_ls[r0 + k]) : 0.f;
+                    }
+                }
+                colsum += csum;
+                kcnt += cnt;
+                // per-head totals (warp reduce, one shared atomic per warp)
+                const int64_t rg = r_first + r0;
+                if (rg / a.w == (rg + 31) / a.w) {
+                    const int tot = __reduce_add_sync(kFull, cnt);
+                    if (lane == 0 && tot) atomicAdd(hcnt + (int)(rg / a.w - head0), tot);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        const bool vis = all_visible || j <= c_lim[r0 + k];
+                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                        const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k]) ? 1 : 0);
+                        if (lane == 0 && tot) atomicAdd(hcnt + (int)((rg + k) / a.w - head0), tot);
+                    }
                 }
             }
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + acc);
+            colbuf[(p * 2 + half) * kN + lane_idx] = colsum;
+            if (a.below_col) kcntbuf[(p * 2 + half) * kN + lane_idx] = kcnt;
             sm100::named_bar_sync(1, kEpiWarps * 32);
-            if (ew < 4) {
-                const int col = ew * 32 + lane;
-                const int64_t j = (int64_t)t * kN + col;
-                if (j < a.n) {
-                    const float* cb = colbuf + p * 4 * kN + col;
-                    colp[j] = ((cb[0] + cb[kN]) + (cb[2 * kN] + cb[3 * kN]));
+            if (half == 0 && j < a.n) {
+                colp[j] = colbuf[(p * 2) * kN + lane_idx] + colbuf[(p * 2 + 1) * kN + lane_idx];
+                if (a.below_col) {
+                    const int kc = kcntbuf[(p * 2) * kN + lane_idx] + kcntbuf[(p * 2 + 1) * kN + lane_idx];
+                    if (kc) atomicAdd(a.below_col + (int64_t)s * a.n + j, kc);
                 }
             }
         }
         // columns no row of this block can see
-        for (int64_t j = (int64_t)T * kN + (ew * 32 + lane); j < a.n; j += kEpiWarps * 32) colp[j] = 0.f;
-        if (row_ok) {
-            if (half == 0) {
-                a.row_max[(int64_t)s * R + r] = st.m;
-                a.row_sum[(int64_t)s * R + r] = st.s;
-            }
-            if (below)
-                atomicAdd(a.below_head + (int64_t)s * a.G + r / a.w, (unsigned long long)below);
-        }
+        for (int64_t jj = (int64_t)T * kN + (ew * 32 + lane); jj < a.n; jj += kEpiWarps * 32) colp[jj] = 0.f;
+        sm100::named_bar_sync(1, kEpiWarps * 32);
+        const int nheads = (int)(r_last / a.w - head0 + 1);
+        for (int h = ew * 32 + lane; h < nheads; h += kEpiWarps * 32)
+            if (hcnt[h]) atomicAdd(a.below_head + (int64_t)s * a.G + head0 + h, (unsigned long long)hcnt[h]);
     }
     sm100::tc_fence_before();
     __syncthreads();

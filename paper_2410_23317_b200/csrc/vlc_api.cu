@@ -104,7 +104,7 @@ int vlc_allocate(const uint64_t* below_head, int32_t batch, int32_t layers, int3
                  int64_t prompt_len, double alpha, double beta_min, double beta_max,
                  int64_t cache_extra, double* gamma, double* gamma_mean, double* beta_pre,
                  double* beta, int64_t* kept_counts, int64_t* kept_off, int64_t* cache_off,
-                 int64_t* chunk_off, int32_t* status, void* stream) {
+                 int32_t* status, void* stream) {
     if (!below_head || !gamma || !gamma_mean || !beta_pre || !beta || !kept_counts || !kept_off ||
         !cache_off || !status)
         return fail(VLC_EINVAL, "allocate: null pointer");
@@ -127,7 +127,6 @@ int vlc_allocate(const uint64_t* below_head, int32_t batch, int32_t layers, int3
     a.beta_min = beta_min; a.beta_max = beta_max; a.cache_extra = cache_extra;
     a.gamma = gamma; a.gamma_mean = gamma_mean; a.beta_pre = beta_pre; a.beta = beta;
     a.kept_counts = kept_counts; a.kept_off = kept_off; a.cache_off = cache_off; a.status = status;
-    a.chunk_off = chunk_off;
     return cuda_status(vlc::launch_allocate(a, (cudaStream_t)stream), "allocate");
 }
 
@@ -135,7 +134,7 @@ int vlc_allocate_from_gamma(const double* gamma_mean, int32_t batch, int32_t lay
                             int32_t kv_heads, int64_t prompt_len, double alpha, double beta_min,
                             double beta_max, int64_t cache_extra, double* beta_pre, double* beta,
                             int64_t* kept_counts, int64_t* kept_off, int64_t* cache_off,
-                            int64_t* chunk_off, int32_t* status, void* stream) {
+                            int32_t* status, void* stream) {
     if (!gamma_mean || !beta_pre || !beta || !kept_counts || !kept_off || !cache_off || !status)
         return fail(VLC_EINVAL, "allocate: null pointer");
     if (!(alpha > 0.0 && alpha <= 1.0)) return fail(VLC_EINVAL, "alpha: must be in (0, 1], got %g", alpha);
@@ -152,7 +151,6 @@ int vlc_allocate_from_gamma(const double* gamma_mean, int32_t batch, int32_t lay
     a.gamma = nullptr; a.gamma_mean = const_cast<double*>(gamma_mean);
     a.beta_pre = beta_pre; a.beta = beta;
     a.kept_counts = kept_counts; a.kept_off = kept_off; a.cache_off = cache_off; a.status = status;
-    a.chunk_off = chunk_off;
     return cuda_status(vlc::launch_allocate(a, (cudaStream_t)stream), "allocate");
 }
 
@@ -199,13 +197,13 @@ int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head
 int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const void* v_new,
                     int64_t kv_stride, void* k_cache, void* v_cache, const int64_t* cache_off,
                     const int64_t* base_len, int64_t step, int32_t batch, int32_t layers,
-                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale,
-                    const int64_t* chunk_off, int32_t* tickets, float* partials, int64_t max_items,
-                    float* out, void* stream) {
-    if (!q || !k_new || !v_new || !k_cache || !v_cache || !cache_off || !base_len || !out || !chunk_off ||
-        !tickets || !partials)
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float* out,
+                    void* stream) {
+    if (!q || !k_new || !v_new || !k_cache || !v_cache || !cache_off || !base_len || !out)
         return fail(VLC_EINVAL, "decode_step: null pointer");
-    if (max_items < 1) return fail(VLC_EINVAL, "decode_step: max_items must be >= 1");
+    if ((reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache) |
+         reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15)
+        return fail(VLC_EINVAL, "decode_step: buffers must be 16-byte aligned");
     if (batch < 1 || layers < 1 || kv_heads < 1 || group < 1 || step < 0)
         return fail(VLC_EINVAL, "decode_step: bad shape");
     if (group > 8) return fail(VLC_EUNSUPPORTED, "decode_step: group size %d > 8", group);
@@ -219,12 +217,7 @@ int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const vo
     a.d = head_dim; a.out = out;
     // reference _core.pyx:257: inv = <float>(1.0 / sqrt(<double> d))
     a.inv_scale = (float)(scale > 0.0 ? scale : 1.0 / std::sqrt((double)head_dim));
-    a.chunk_off = chunk_off; a.tickets = tickets; a.partials = partials; a.max_items = max_items;
     return cuda_status(vlc::launch_decode(a, (cudaStream_t)stream), "decode_step");
-}
-
-int64_t vlc_decode_max_items(int64_t max_kept_rows, int64_t slots, int64_t cache_extra) {
-    return (max_kept_rows + slots * cache_extra) / vlc::kDecodeChunk + 2 * slots;
 }
 
 }  // extern "C"

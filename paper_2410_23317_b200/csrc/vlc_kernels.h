@@ -7,7 +7,8 @@
 
 namespace vlc {
 
-constexpr int kDecodeChunk = 64;   // keys per K5 work item
+constexpr int kDecodeChunk = 32;   // keys per K5 bulk-copy stage
+constexpr int kDecodeCluster = 8;  // CTAs per (b, l, kv) slot in K5 (one cluster)
 
 // K1: post-vision attention statistics for every (b, l, kv) slot.
 // Slot s = (b*L + l)*Hkv + kv owns window rows [s*R, s*R + R), R = G*w, i.e.
@@ -44,7 +45,6 @@ struct BudgetArgs {
     int64_t* kept_counts;      // [B, L]
     int64_t* kept_off;         // [B*L*Hkv + 1]  prefix of kept counts per slot
     int64_t* cache_off;        // [B*L*Hkv + 1]  prefix of (kept + cache_extra)
-    int64_t* chunk_off;        // optional [B*L*Hkv + 1] prefix of K5 work items per slot
     int* status;               // [B]  0 ok, 1 degenerate (Z == 0)
 };
 cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st);
@@ -96,10 +96,6 @@ struct DecodeArgs {
     int slots, Hkv, L, G, d;
     float inv_scale;
     float* out;                // f32 [B*L*Hq, d]
-    const int64_t* chunk_off;  // [slots + 1] work items (kDecodeChunk keys) per slot
-    int* tickets;              // [slots] zero-initialised completion counters
-    float* partials;           // [items, G, d + 2]
-    int64_t max_items;         // host bound on chunk_off[slots] (grid sizing)
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 

@@ -130,7 +130,6 @@ class VLCache:
         self.kept_counts = torch.empty(s.B * s.L, dtype=i64, device=dev)
         self.kept_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
         self.cache_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
-        self.chunk_off = torch.zeros(s.slots + 1, dtype=i64, device=dev)
         self.status = torch.zeros(s.B, dtype=i32, device=dev)
         self.max_rows = kept_rows_bound(s.B, s.L, s.Hkv, s.m, alpha, beta_min)
         self.kept_idx = torch.empty(self.max_rows, dtype=i32, device=dev)
@@ -142,10 +141,6 @@ class VLCache:
         self.k_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.v_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty(s.B * s.L * s.Hq * s.d, dtype=f32, device=dev)
-        # K5 split-K workspace: work items of kDecodeChunk keys, per-slot tickets
-        self.max_items = int(_lib.load().vlc_decode_max_items(self.max_rows, s.slots, self.decode_steps))
-        self.tickets = torch.zeros(s.slots, dtype=i32, device=dev)
-        self.partials = torch.empty(self.max_items * s.G * (s.d + 2), dtype=f32, device=dev)
         self._graphs = {}
 
     # ------------------------------------------------------------ stages
@@ -180,8 +175,7 @@ class VLCache:
         _lib.call("vlc_allocate", _ptr(self.below_alloc), s.B, s.L, self.hq_alloc, s.Hkv, s.w, s.m, s.m - s.w,
                   s.m, self.alpha, self.beta_min, self.beta_max, self.decode_steps, _ptr(self.gamma),
                   _ptr(self.gamma_mean), _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
-                  _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.chunk_off), _ptr(self.status),
-                  _stream())
+                  _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.status), _stream())
 
     def select(self):
         s = self.shape
@@ -235,8 +229,8 @@ class VLCache:
         _lib.call("vlc_decode_step", q_dec.data_ptr() + step * s.d * esz, n_dec * s.d,
                   keys.data_ptr() + (s.m + step) * s.d * esz, values.data_ptr() + (s.m + step) * s.d * esz,
                   T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.cache_off),
-                  _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, _ptr(self.chunk_off),
-                  _ptr(self.tickets), _ptr(self.partials), self.max_items, _ptr(self.out), _stream())
+                  _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, _ptr(self.out),
+                  _stream())
         return self.out
 
     def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None):
