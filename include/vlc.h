@@ -130,11 +130,13 @@ VLC_API int vlc_gather(const void *keys, const void *values, int32_t slots, int3
  * _core.pyx:245-278).  q head (b,l,h) is at q + ((b*L+l)*Hq+h)*q_stride,
  * slot s's new row at k_new/v_new + s*kv_stride (elements).  out: f32
  * [B*L*Hq, head_dim].  head_dim in {64, 128}, G <= 8; scale as in K1.
- * No workspace: each slot is split across an 8-CTA cluster that merges its
- * partial softmax states through distributed shared memory.
+ * k_cache / v_cache: bf16 [cache_rows, head_dim], 16-byte aligned, rows that
+ * no step has written yet must hold finite values (zero-initialise once).
+ * No workspace; one CTA per slot.
  */
 VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, const void *v_new,
-                    int64_t kv_stride, void *k_cache, void *v_cache, const int64_t *cache_off,
+                    int64_t kv_stride, void *k_cache, void *v_cache, int64_t cache_rows,
+                    const int64_t *cache_off,
                     const int64_t *base_len, int64_t step, int32_t batch, int32_t layers,
                     int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float *out,
                     void *stream);

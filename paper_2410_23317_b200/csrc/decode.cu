@@ -4,15 +4,19 @@
 // then decode_step over the first k + s + 1 rows for the G query heads of each
 // KV head) and _core.pyx:245-278 (decode_step: softmax(q K^T / sqrt(d)) V, fp32).
 //
-// One CTA per (b, l, kv) slot streams the slot's K and V rows (contiguous in
-// its cache segment) through a kStages-deep shared-memory ring filled by 1-D
-// TMA bulk copies, so ~kStages*16 KB per CTA are always in flight without
-// occupying registers.  Each 32-row chunk is reduced in three short phases:
-// (A) logits, one K-row load shared by all G query heads (GQA-aware: every key
-// row is read from HBM once per step for the whole group); (B) per-head online
-// softmax update, one warp per head; (C) P.V with threads over (head, dims).
-// No workspace and no cross-CTA merge.  The chunk holding row k + step takes it
-// from k_new / v_new and also appends it to the cache for later steps.
+// One CTA per (b, l, kv) slot streams the slot's K and V rows through a
+// kStages-deep shared-memory ring of 64-row chunks, loaded by 2-D TMA with the
+// 128-byte swizzle so tensor-core fragments come out of shared memory
+// conflict-free.  The G <= 8 query heads of the KV head form the M rows of
+// mma.sync tiles (GQA: every key row is read from HBM once per step for the
+// whole group):
+//   S = Q K^T     m16n8k16, bf16 in, fp32 accumulate (exact products);
+//   O += P V      m16n8k8, P split into bf16 hi + lo parts (~2^-16 relative),
+//                 V exact bf16, fp32 accumulate.
+// Each of the 8 warps owns 8 rows of every chunk with its own online-softmax
+// state; the warps' (max, sum, O) partials merge once at the end.  The chunk
+// holding row k + step takes it from k_new / v_new (patched into the swizzled
+// tile) and also appends it to the cache for later steps.
 #include "sm100.cuh"
 #include "vlc_common.cuh"
 #include "vlc_kernels.h"
@@ -23,202 +27,232 @@ namespace {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
-constexpr int kChunk = 32;     // rows per ring stage
-constexpr int kStages = 4;
+constexpr int kChunk = 64;      // rows per ring stage (8 per warp)
+constexpr int kStages = 3;
 
-template <int D, int G>
+template <int D>
 struct Cfg {
-    static constexpr int LPK = D / 8;                  // lanes per key row (16-byte pieces)
-    static constexpr int KPI = 32 / LPK;               // keys per warp instruction
-    static constexpr int UNITS = kChunk / KPI;         // key groups per chunk
-    static constexpr int UPW = UNITS / kWarps;         // key groups per warp
-    static constexpr int DP = D / 2;                   // dim pairs
-    static constexpr int HSTRIDE = kThreads / DP;      // heads covered per thread sweep
-    static constexpr int HPT = (G + HSTRIDE - 1) / HSTRIDE;   // heads per thread in phase C
-    static constexpr uint32_t kRowBytes = D * 2;
-    static constexpr uint32_t kStageBytes = kChunk * kRowBytes;
-    static constexpr uint32_t kBytes = 2 * kStages * kStageBytes;
-    static_assert(UNITS % kWarps == 0, "chunk must split evenly over the warps");
+    static constexpr int KB = D / 64;                        // 64-dim (128 B) swizzle boxes per row
+    static constexpr uint32_t kBox = kChunk * 128;           // bytes of one box (64 rows x 128 B)
+    static constexpr uint32_t kTile = KB * kBox;             // K (or V) tile of a chunk
+    static constexpr uint32_t kStage = 2 * kTile;            // K + V
+    static constexpr uint32_t kBytes = kStages * kStage + 1024;   // + alignment slack
+    static constexpr int NT = D / 8;                         // 8-dim output tiles
 };
 
-VLC_DEV void unpack8(const uint4& u, float (&f)[8]) {
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) { f[2 * e] = bf16_lo(w[e]); f[2 * e + 1] = bf16_hi(w[e]); }
+// byte offset of 16-byte piece `c` (of the row's D/8) of row r inside a tile
+template <int D>
+VLC_DEV uint32_t swz(int r, int c) {
+    return (uint32_t)((c >> 3) * Cfg<D>::kBox + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
+VLC_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+VLC_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+// D = A(16x16, rows 8..15 zero) * B(16x8) + C, bf16 -> f32
+VLC_DEV void mma_k16(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+// D = A(16x8, rows 8..15 zero) * B(8x8) + C
+VLC_DEV void mma_k8(float (&d)[4], uint32_t a0, uint32_t b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(0u), "r"(b0));
+}
+VLC_DEV uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+VLC_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads) decode_kernel(DecodeArgs a) {
-    using C = Cfg<D, G>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* kring = smem;                                   // [kStages][kChunk][D] bf16
-    uint8_t* vring = smem + kStages * C::kStageBytes;        // [kStages][kChunk][D] bf16
-    __shared__ float lg[G][kChunk];                          // logits, then probabilities
-    __shared__ float h_scale[G], h_sum[G];
+__global__ void __launch_bounds__(kThreads, 2)
+decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, DecodeArgs a) {
+    using C = Cfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar[kStages];
+    __shared__ float part_m[kWarps][kMaxG], part_s[kWarps][kMaxG];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int pc = lane % C::LPK, sub = lane / C::LPK;
+    const int row = lane >> 2, quad = lane & 3;              // fragment row (query head), column pair
     const int s = blockIdx.x;
-    const int64_t n = a.base_len[s / a.Hkv] + a.step + 1;   // rows this step
+    const int64_t n = a.base_len[s / a.Hkv] + a.step + 1;    // rows this step
     const int64_t new_row = n - 1;
+    const int64_t seg = a.cache_off[s];
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
-    const size_t seg = (size_t)a.cache_off[s] * C::kRowBytes;
-    const uint8_t* kc = static_cast<const uint8_t*>(a.k_cache) + seg;
-    const uint8_t* vc = static_cast<const uint8_t*>(a.v_cache) + seg;
 
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) sm100::mbar_init(&bar[i], 1);
         sm100::fence_barrier_init();
+        sm100::tma_prefetch(&kmap);
+        sm100::tma_prefetch(&vmap);
     }
     __syncthreads();
-    auto issue = [&](int c) {   // rows of chunk c already in the cache (not the new row)
+    auto issue = [&](int c) {
         const int st = c % kStages;
-        const int64_t j0 = (int64_t)c * kChunk;
-        const int64_t j1 = imin(j0 + kChunk, new_row);
-        const uint32_t bytes = j1 > j0 ? (uint32_t)(j1 - j0) * C::kRowBytes : 0u;
-        sm100::fence_proxy_async();
-        sm100::mbar_expect_tx(&bar[st], 2 * bytes);
-        if (bytes) {
-            sm100::bulk_load(kring + st * C::kStageBytes, kc + j0 * C::kRowBytes, bytes, &bar[st]);
-            sm100::bulk_load(vring + st * C::kStageBytes, vc + j0 * C::kRowBytes, bytes, &bar[st]);
+        uint8_t* kdst = smem + st * C::kStage;
+        const int y = (int)(seg + (int64_t)c * kChunk);
+        sm100::mbar_expect_tx(&bar[st], C::kStage);
+        for (int kb = 0; kb < C::KB; ++kb) {
+            sm100::tma_load_2d(kdst + kb * C::kBox, &kmap, &bar[st], kb * 64, y);
+            sm100::tma_load_2d(kdst + C::kTile + kb * C::kBox, &vmap, &bar[st], kb * 64, y);
         }
     };
     if (tid == 0)
         for (int c = 0; c < kStages && c < nchunks; ++c) issue(c);
 
-    // query pieces of every head for phase A (this lane's 8 dims)
-    const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(a.q);
-    float q[G][8];
+    // Q as A fragments (rows = heads; rows >= G and 8..15 are zero), per 16-dim k-step
+    const uint32_t* qw = reinterpret_cast<const uint32_t*>(a.q);
+    uint32_t qa[D / 16][2];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(qb + ((int64_t)s * G + g) * a.q_stride + pc * 8), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) q[g][e] = f[e] * a.inv_scale;
+    for (int kk = 0; kk < D / 16; ++kk) {
+        if (row < G) {
+            const int64_t base = (((int64_t)s * G + row) * a.q_stride + kk * 16) / 2;
+            qa[kk][0] = qw[base + quad];
+            qa[kk][1] = qw[base + 4 + quad];
+        } else {
+            qa[kk][0] = qa[kk][1] = 0u;
+        }
     }
-    // phase-C ownership: dim pair dp, heads gb, gb + HSTRIDE, ...
-    const int dp = tid % C::DP, gb = tid / C::DP;
-    float acc[C::HPT][2];
+    float o[C::NT][4];
 #pragma unroll
-    for (int h = 0; h < C::HPT; ++h) acc[h][0] = acc[h][1] = 0.f;
-    // phase-B state (warp g owns head g)
-    float run_m = -INFINITY, run_s = 0.f;
+    for (int t = 0; t < C::NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+    float run_m = -INFINITY, run_s = 0.f;                    // head `row`, this thread's columns
+    const float c1 = a.inv_scale * kLog2e;
 
     for (int c = 0; c < nchunks; ++c) {
         const int st = c % kStages;
         const int64_t j0 = (int64_t)c * kChunk;
-        const int nk = (int)imin(kChunk, n - j0);
-        uint8_t* ks = kring + st * C::kStageBytes;
-        uint8_t* vs = vring + st * C::kStageBytes;
-        if (new_row < j0 + kChunk) {   // last chunk: bring in the new row (CTA-uniform)
-            if (tid < 2 * C::LPK) {
-                const bool isv = tid >= C::LPK;
-                const int piece = tid % C::LPK;
+        uint8_t* ks = smem + st * C::kStage;
+        uint8_t* vs = ks + C::kTile;
+        sm100::mbar_wait(&bar[st], (c / kStages) & 1);
+        if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (CTA-uniform)
+            const int r = (int)(new_row - j0);
+            if (tid < 2 * (D / 8)) {
+                const bool isv = tid >= D / 8;
+                const int piece = tid % (D / 8);
                 const uint4 val = reinterpret_cast<const uint4*>(
                     static_cast<const __nv_bfloat16*>(isv ? a.v_new : a.k_new) + (int64_t)s * a.kv_stride)[piece];
-                reinterpret_cast<uint4*>((isv ? vs : ks) + (new_row - j0) * C::kRowBytes)[piece] = val;
-                reinterpret_cast<uint4*>(static_cast<uint8_t*>(isv ? a.v_cache : a.k_cache) + seg +
-                                         new_row * C::kRowBytes)[piece] = val;
+                *reinterpret_cast<uint4*>((isv ? vs : ks) + swz<D>(r, piece)) = val;
+                reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(isv ? a.v_cache : a.k_cache) +
+                                         (seg + new_row) * D)[piece] = val;
             }
             __syncthreads();
         }
-        sm100::mbar_wait(&bar[st], (c / kStages) & 1);
-
-        // ---- A: logits; each K-row piece is loaded once for all G heads
+        // ---- S = Q K^T for this warp's 8 rows (keys) of the chunk
+        const int kr = warp * 8;                               // first key of the warp
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t kbase = sm100::smem_u32(ks);
 #pragma unroll
-        for (int u = 0; u < C::UPW; ++u) {
-            const int kk = (warp + u * kWarps) * C::KPI + sub;
-            float kf[8];
-            unpack8(reinterpret_cast<const uint4*>(ks + kk * C::kRowBytes)[pc], kf);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                float dot = 0.f;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) dot = fmaf(q[g][e], kf[e], dot);
-#pragma unroll
-                for (int o = C::LPK / 2; o >= 1; o >>= 1) dot += __shfl_xor_sync(kFull, dot, o);
-                if (pc == 0) lg[g][kk] = kk < nk ? dot : -INFINITY;
-            }
+        for (int kk = 0; kk < D / 16; kk += 2) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kbase + swz<D>(kr + (lane & 7), kk * 2 + (lane >> 3)), b0, b1, b2, b3);
+            mma_k16(sacc, qa[kk][0], qa[kk][1], b0, b1);
+            mma_k16(sacc, qa[kk + 1][0], qa[kk + 1][1], b2, b3);
         }
-        __syncthreads();
-        // ---- B: online softmax update per head (warp g)
-        if (warp < G) {
-            const float l = lg[warp][lane];
-            const float mn = fmaxf(run_m, warp_max(l));      // finite: row 0 of the chunk is valid
-            const float p = ex2((l - mn) * kLog2e);
-            const float sc = ex2((run_m - mn) * kLog2e);       // 0 on the first chunk
-            lg[warp][lane] = p;
-            run_s = run_s * sc + warp_sum(p);
-            run_m = mn;
-            if (lane == 0) { h_scale[warp] = sc; h_sum[warp] = run_s; }
-        }
-        __syncthreads();
-        // ---- C: acc = acc * scale + P.V over the chunk
+        // ---- online softmax of head `row` over keys kr + 2*quad, +1
+        const int64_t jk = j0 + kr + 2 * quad;
+        const float l0 = jk < n ? sacc[0] : -INFINITY;
+        const float l1 = jk + 1 < n ? sacc[1] : -INFINITY;
+        float tm = fmaxf(l0, l1);
+        tm = fmaxf(tm, __shfl_xor_sync(kFull, tm, 1));
+        tm = fmaxf(tm, __shfl_xor_sync(kFull, tm, 2));
+        const float mn = fmaxf(run_m, tm);
+        const float mnb = mn == -INFINITY ? 0.f : mn * c1;    // rows of an empty tail chunk
+        const float p0 = ex2(fmaf(l0, c1, -mnb));
+        const float p1 = ex2(fmaf(l1, c1, -mnb));
+        if (__any_sync(kFull, mn != run_m)) {
+            const float sc = run_m == -INFINITY ? 0.f : ex2(fmaf(run_m, c1, -mnb));
 #pragma unroll
-        for (int h = 0; h < C::HPT; ++h) {
-            const int g = gb + h * C::HSTRIDE;
-            if (g < G) {
-                const float sc = h_scale[g];
-                float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
-                if (nk == kChunk) {
-#pragma unroll 8
-                    for (int kk = 0; kk < kChunk; kk += 2) {
-                        const uint32_t u0 = reinterpret_cast<const uint32_t*>(vs + kk * C::kRowBytes)[dp];
-                        const uint32_t u1 = reinterpret_cast<const uint32_t*>(vs + (kk + 1) * C::kRowBytes)[dp];
-                        const float p0 = lg[g][kk], p1 = lg[g][kk + 1];
-                        a0 = fmaf(p0, bf16_lo(u0), a0);
-                        a1 = fmaf(p0, bf16_hi(u0), a1);
-                        b0 = fmaf(p1, bf16_lo(u1), b0);
-                        b1 = fmaf(p1, bf16_hi(u1), b1);
-                    }
-                } else {   // rows past nk hold stale bytes: never touch them
-                    for (int kk = 0; kk < nk; ++kk) {
-                        const uint32_t u0 = reinterpret_cast<const uint32_t*>(vs + kk * C::kRowBytes)[dp];
-                        const float p0 = lg[g][kk];
-                        a0 = fmaf(p0, bf16_lo(u0), a0);
-                        a1 = fmaf(p0, bf16_hi(u0), a1);
-                    }
-                }
-                acc[h][0] = fmaf(acc[h][0], sc, a0 + b0);
-                acc[h][1] = fmaf(acc[h][1], sc, a1 + b1);
-            }
+            for (int t = 0; t < C::NT; ++t) { o[t][0] *= sc; o[t][1] *= sc; }
+            run_s *= sc;
         }
-        __syncthreads();   // stage and logits free
+        run_m = mn;
+        run_s += p0 + p1;
+        // P as the A operand of m16n8k8: hi + lo bf16 parts
+        const float h0 = bf16_round(p0), h1 = bf16_round(p1);
+        const uint32_t phi = pack_bf16(h0, h1);
+        const uint32_t plo = pack_bf16(p0 - h0, p1 - h1);
+        // ---- O += P V over the warp's 8 keys, 8-dim output tiles
+        const uint32_t vbase = sm100::smem_u32(vs);
+#pragma unroll
+        for (int t = 0; t < C::NT; t += 4) {
+            uint32_t v0, v1, v2, v3;
+            ldsm_x4_t(vbase + swz<D>(kr + (lane & 7), t + (lane >> 3)), v0, v1, v2, v3);
+            mma_k8(o[t], phi, v0);     mma_k8(o[t], plo, v0);
+            mma_k8(o[t + 1], phi, v1); mma_k8(o[t + 1], plo, v1);
+            mma_k8(o[t + 2], phi, v2); mma_k8(o[t + 2], plo, v2);
+            mma_k8(o[t + 3], phi, v3); mma_k8(o[t + 3], plo, v3);
+        }
+        __syncthreads();                                       // stage consumed by every warp
         if (tid == 0 && c + kStages < nchunks) issue(c + kStages);
     }
+
+    // ---- merge the 8 warps: per head, (max, sum) then O, through shared memory
+    run_s += __shfl_xor_sync(kFull, run_s, 1);
+    run_s += __shfl_xor_sync(kFull, run_s, 2);
+    if (quad == 0 && row < G) { part_m[warp][row] = run_m; part_s[warp][row] = run_s; }
+    float* po = reinterpret_cast<float*>(smem);               // [kWarps][G][D], ring is idle now
+    if (row < G) {
 #pragma unroll
-    for (int h = 0; h < C::HPT; ++h) {
-        const int g = gb + h * C::HSTRIDE;
-        if (g < G) {
-            const float inv = 1.f / h_sum[g];
-            float2 o = make_float2(acc[h][0] * inv, acc[h][1] * inv);
-            reinterpret_cast<float2*>(a.out + ((int64_t)s * G + g) * D)[dp] = o;
+        for (int t = 0; t < C::NT; ++t)
+            *reinterpret_cast<float2*>(po + (warp * G + row) * D + t * 8 + 2 * quad) = make_float2(o[t][0], o[t][1]);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < G * D; idx += kThreads) {
+        const int g = idx / D, dim = idx % D;
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, part_m[w][g]);
+        float S = 0.f, O = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            if (part_m[w][g] == -INFINITY) continue;
+            const float f = ex2((part_m[w][g] - M) * c1);
+            S = fmaf(part_s[w][g], f, S);
+            O = fmaf(po[(w * G + g) * D + dim], f, O);
         }
+        a.out[((int64_t)s * G + g) * D + dim] = O / S;
     }
 }
 
 template <int D, int G>
-cudaError_t launch_dg(const DecodeArgs& a, cudaStream_t st) {
-    using C = Cfg<D, G>;
+cudaError_t launch_dg(const DecodeArgs& a, const CUtensorMap& km, const CUtensorMap& vm, cudaStream_t st) {
+    using C = Cfg<D>;
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::kBytes);
     if (e != cudaSuccess) return e;
-    decode_kernel<D, G><<<a.slots, kThreads, C::kBytes, st>>>(a);
+    decode_kernel<D, G><<<a.slots, kThreads, C::kBytes, st>>>(km, vm, a);
     return cudaGetLastError();
 }
 
 template <int D>
 cudaError_t launch_d(const DecodeArgs& a, cudaStream_t st) {
+    CUtensorMap km, vm;
+    if (!make_tmap_2d(&km, a.k_cache, a.cache_rows, D, kChunk) ||
+        !make_tmap_2d(&vm, a.v_cache, a.cache_rows, D, kChunk))
+        return cudaErrorInvalidValue;
     switch (a.G) {
-        case 1: return launch_dg<D, 1>(a, st);
-        case 2: return launch_dg<D, 2>(a, st);
-        case 3: return launch_dg<D, 3>(a, st);
-        case 4: return launch_dg<D, 4>(a, st);
-        case 5: return launch_dg<D, 5>(a, st);
-        case 6: return launch_dg<D, 6>(a, st);
-        case 7: return launch_dg<D, 7>(a, st);
-        case 8: return launch_dg<D, 8>(a, st);
+        case 1: return launch_dg<D, 1>(a, km, vm, st);
+        case 2: return launch_dg<D, 2>(a, km, vm, st);
+        case 3: return launch_dg<D, 3>(a, km, vm, st);
+        case 4: return launch_dg<D, 4>(a, km, vm, st);
+        case 5: return launch_dg<D, 5>(a, km, vm, st);
+        case 6: return launch_dg<D, 6>(a, km, vm, st);
+        case 7: return launch_dg<D, 7>(a, km, vm, st);
+        case 8: return launch_dg<D, 8>(a, km, vm, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -19,8 +19,6 @@
 // The score matrix never leaves the SM: TMEM -> registers -> statistics.
 #include <cuda.h>
 
-#include <mutex>
-
 #include "score_epilogue.cuh"
 #include "sm100.cuh"
 #include "vlc_kernels.h"
@@ -315,42 +313,12 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 }
 
 // ---------------------------------------------------------------- host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    });
-    return fn;
-}
-
-// 2-D bf16 map over [rows, d]: box = 64 elements (128 B, swizzled) x box_rows
-bool make_map(CUtensorMap* map, const void* base, int64_t rows, int d, int box_rows) {
-    EncodeTiledFn enc = encode_fn();
-    if (!enc) return false;
-    cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-    cuuint64_t gstride[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-    cuuint32_t estride[2] = {1, 1};
-    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int D>
 cudaError_t launch_tc(const ScoreArgs& a, int nrb, cudaStream_t st) {
     CUtensorMap qmap, kmap;
     const int64_t R = (int64_t)a.G * a.w;
-    if (!make_map(&qmap, a.q, (int64_t)a.slots * R, a.d, kM)) return cudaErrorInvalidValue;
-    if (!make_map(&kmap, a.k, (int64_t)a.slots * a.T, a.d, kN)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&qmap, a.q, (int64_t)a.slots * R, a.d, kM)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&kmap, a.k, (int64_t)a.slots * a.T, a.d, kN)) return cudaErrorInvalidValue;
     const size_t sm = Layout<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;

@@ -195,7 +195,8 @@ int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head
 }
 
 int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const void* v_new,
-                    int64_t kv_stride, void* k_cache, void* v_cache, const int64_t* cache_off,
+                    int64_t kv_stride, void* k_cache, void* v_cache, int64_t cache_rows,
+                    const int64_t* cache_off,
                     const int64_t* base_len, int64_t step, int32_t batch, int32_t layers,
                     int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float* out,
                     void* stream) {
@@ -213,6 +214,8 @@ int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const vo
     vlc::DecodeArgs a{};
     a.q = q; a.q_stride = q_stride; a.k_new = k_new; a.v_new = v_new; a.kv_stride = kv_stride;
     a.k_cache = k_cache; a.v_cache = v_cache; a.cache_off = cache_off; a.base_len = base_len;
+    a.cache_rows = cache_rows;
+    if (cache_rows < 1) return fail(VLC_EINVAL, "decode_step: cache_rows must be >= 1");
     a.step = step; a.slots = batch * layers * kv_heads; a.Hkv = kv_heads; a.L = layers; a.G = group;
     a.d = head_dim; a.out = out;
     // reference _core.pyx:257: inv = <float>(1.0 / sqrt(<double> d))

@@ -3,9 +3,14 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace vlc {
+
+// 2-D bf16 TMA map over [rows, d] (row-major): box = 64 elements (one 128-byte
+// swizzle row) x box_rows, SWIZZLE_128B.  False if the driver entry is missing.
+bool make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int d, int box_rows);
 
 constexpr int kDecodeChunk = 32;   // keys per K5 bulk-copy stage
 constexpr int kDecodeCluster = 8;  // CTAs per (b, l, kv) slot in K5 (one cluster)
@@ -96,6 +101,7 @@ struct DecodeArgs {
     int slots, Hkv, L, G, d;
     float inv_scale;
     float* out;                // f32 [B*L*Hq, d]
+    int64_t cache_rows;        // rows of k_cache / v_cache (TMA bounds)
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 

@@ -138,8 +138,9 @@ class VLCache:
         self.key_scratch = (torch.empty(s.slots * s.m, dtype=i64, device=dev)
                             if s.m > 24 * 1024 else None)
         self.cache_rows = self.max_rows + s.slots * self.decode_steps
-        self.k_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
-        self.v_cache = torch.empty(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
+        # zero-initialised: K5 tiles may cover rows no step has written yet
+        self.k_cache = torch.zeros(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
+        self.v_cache = torch.zeros(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty(s.B * s.L * s.Hq * s.d, dtype=f32, device=dev)
         self._graphs = {}
 
@@ -228,7 +229,7 @@ class VLCache:
         esz = 2
         _lib.call("vlc_decode_step", q_dec.data_ptr() + step * s.d * esz, n_dec * s.d,
                   keys.data_ptr() + (s.m + step) * s.d * esz, values.data_ptr() + (s.m + step) * s.d * esz,
-                  T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.cache_off),
+                  T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), self.cache_rows, _ptr(self.cache_off),
                   _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, _ptr(self.out),
                   _stream())
         return self.out
