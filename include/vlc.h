@@ -50,16 +50,18 @@ VLC_API const char *vlc_last_error(void);
  * _core.pyx:201-204 is exactly "l - max < t*". */
 VLC_API float vlc_threshold_logit(double p);
 
-/* Rows of col_partial per slot for a window of `rows` = G*w rows. */
-VLC_API int64_t vlc_score_row_blocks(int64_t rows);
+/* Rows of col_partial per slot for a window of `rows` = G*w rows (one
+ * partial per 32 window rows; 4 per 128-row block). */
+VLC_API int64_t vlc_score_partials(int64_t rows);
 
 /*
  * K1 score_stats.  Replaces _kernels.stats_tiled (reference _core.pyx:210-242)
  * for all G heads of every slot: causal logits q.k/sqrt(d) of window row
  * (absolute index q_base + i) against keys [0, min(n_keys, q_base+i+1)).
  *   row_max, row_sum : f32 [slots*G*w]       (_core.pyx:142-155)
- *   col_partial      : f32 [slots, nrb, n_keys] column mass of each 128-row
- *                      block; per-head col_score when G == 1 and nrb == 1
+ *   col_partial      : f32 [slots, vlc_score_partials(G*w), n_keys] column
+ *                      mass of each 32-row group (their sum is the slot's
+ *                      col_score summed over its G heads)
  *   below_head       : u64 [slots*G]  entries with exp(l - max) < p, per head
  *   below_col        : i32 [slots, n_keys] or NULL (per-column counts)
  * scale <= 0 selects 1/sqrt(head_dim) (zero-padded operands pass the true d's).

@@ -48,7 +48,7 @@ def stats_tiled(q, keys, q_base, p, tile):
     dp = 64 if d <= 64 else 128   # K1 tiles are 64/128 wide; zero columns add nothing
     qd = to_device_bf16(_padded(q, dp))
     kd = to_device_bf16(_padded(keys, dp))
-    nrb = int(_lib.load().vlc_score_row_blocks(w))
+    nrb = int(_lib.load().vlc_score_partials(w))
     f32 = dict(dtype=torch.float32, device="cuda")
     row_max = torch.empty(w, **f32)
     row_sum = torch.empty(w, **f32)

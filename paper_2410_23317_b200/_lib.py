@@ -28,7 +28,7 @@ _SIGNATURES = {
     "vlc_strerror": (ctypes.c_char_p, [ctypes.c_int]),
     "vlc_last_error": (ctypes.c_char_p, []),
     "vlc_threshold_logit": (ctypes.c_float, [_F64]),
-    "vlc_score_row_blocks": (_I64, [_I64]),
+    "vlc_score_partials": (_I64, [_I64]),
     "vlc_score_stats": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64,
                                        _F64, _P, _P, _P, _P, _P, _P]),
     "vlc_allocate": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64, _F64,

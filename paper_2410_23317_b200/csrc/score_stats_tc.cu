@@ -19,7 +19,7 @@
 // The score matrix never leaves the SM: TMEM -> registers -> statistics.
 #include <cuda.h>
 
-#include "score_epilogue.cuh"
+#include "vlc_common.cuh"
 #include "sm100.cuh"
 #include "vlc_kernels.h"
 
@@ -29,7 +29,7 @@ namespace {
 constexpr int kM = 128;          // window rows per CTA (UMMA M)
 constexpr int kN = 128;          // keys per tile (UMMA N)
 constexpr int kStages = 3;       // K tile ring
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;    // 4 per TMEM lane quarter, one 32-column group each
 constexpr int kThreads = 128 + kEpiWarps * 32;
 constexpr uint32_t kTmemCols = 2 * kN;
 
@@ -41,10 +41,8 @@ struct Layout {
     static constexpr uint32_t kQBytes = KB * kQRegion;
     static constexpr uint32_t kKBytes = KB * kKRegion;      // one stage
     static constexpr uint32_t kBarOff = kQBytes + kStages * kKBytes;
-    static constexpr uint32_t kColOff = kBarOff + 256;               // f32 [2 parity][2 half][kN]
-    static constexpr uint32_t kKcntOff = kColOff + 4 * kN * 4;       // i32 [2][2][kN]
-    static constexpr uint32_t kRowOff = kKcntOff + 4 * kN * 4;       // float2 [2 half][kM]
-    static constexpr uint32_t kConstOff = kRowOff + 2 * kM * 8;      // mb, ls, t2 f32 + lim i32, [kM] each
+    static constexpr uint32_t kRowOff = kBarOff + 256;               // float2 [4 column groups][kM]
+    static constexpr uint32_t kConstOff = kRowOff + 4 * kM * 8;      // mb, ls, t2 f32 + lim i32, [kM] each
     static constexpr uint32_t kHcntOff = kConstOff + 4 * kM * 4;     // i32 [kM] head counters
     static constexpr uint32_t kBytes = kHcntOff + kM * 4 + 1024;     // + alignment slack
 };
@@ -59,7 +57,7 @@ VLC_DEV float max32(const float (&l)[32]) {
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-               ScoreArgs a, int nrb) {
+               ScoreArgs a, int nparts) {
     using LY = Layout<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -70,8 +68,6 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     uint64_t* tfull = qfull + 1;              // [2]
     uint64_t* tempty = tfull + 2;             // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float* colbuf = reinterpret_cast<float*>(smem + LY::kColOff);
-    int* kcntbuf = reinterpret_cast<int*>(smem + LY::kKcntOff);
     float2* rowstat = reinterpret_cast<float2*>(smem + LY::kRowOff);
     float* c_mb = reinterpret_cast<float*>(smem + LY::kConstOff);    // row max (raw dot) * c1
     float* c_ls = c_mb + kM;                                          // log2(row sum)
@@ -154,9 +150,10 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        const int ew = warp - 4, sub = warp & 3, half = ew >> 2;
+        // warp -> (TMEM lane quarter `sub`, 32-column group `cg`)
+        const int ew = warp - 4, sub = warp & 3, cg = ew >> 2;
         const int lane_idx = 32 * sub + lane;                  // TMEM lane of this thread
-        const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16);
+        const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + cg * 32;
         const float c1 = a.inv_scale * kLog2e;
         float l[32];
 
@@ -171,47 +168,47 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 const int acc = it & 1;
                 sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
                 sm100::tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int col0 = half * 64 + c * 32;
-                    sm100::tmem_ld32(lane_addr + acc * kN + col0, l);
-                    const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + col0)));
-                    const bool full_chunk = __all_sync(kFull, valid == 32);
-                    float cmax;
-                    if (full_chunk) {
-                        cmax = max32(l);
-                    } else {
-                        cmax = -INFINITY;
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
-                    }
-                    if (cmax > m) {
-                        sum *= ex2((m - cmax) * c1);   // 0 while m == -inf
-                        m = cmax;
-                    }
-                    const float mb = m * c1;
-                    float acc_s = 0.f;
-                    if (full_chunk) {
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
-                    }
-                    sum += acc_s;
-                }
+                sm100::tmem_ld32(lane_addr + acc * kN, l);
                 sm100::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + acc);
+                if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the chunk now
+                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
+                const bool full_chunk = __all_sync(kFull, valid == 32);
+                float cmax;
+                if (full_chunk) {
+                    cmax = max32(l);
+                } else {
+                    cmax = -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+                }
+                if (cmax > m) {
+                    sum *= ex2((m - cmax) * c1);   // 0 while m == -inf
+                    m = cmax;
+                }
+                const float mb = m * c1;
+                float acc_s = 0.f;
+                if (full_chunk) {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                }
+                sum += acc_s;
             }
-            rowstat[half * kM + lane_idx] = make_float2(m, sum);
+            rowstat[cg * kM + lane_idx] = make_float2(m, sum);
             sm100::named_bar_sync(1, kEpiWarps * 32);
-            if (half == 0) {
-                const float2 h0 = rowstat[lane_idx], h1 = rowstat[kM + lane_idx];
-                const float M = fmaxf(h0.x, h1.x);
+            if (cg == 0) {
+                float M = -INFINITY;
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
                 float S = 0.f;
-                if (h0.x != -INFINITY) S += h0.y * ex2((h0.x - M) * c1);
-                if (h1.x != -INFINITY) S += h1.y * ex2((h1.x - M) * c1);
+#pragma unroll
+                for (int g4 = 0; g4 < 4; ++g4) {
+                    const float2 h = rowstat[g4 * kM + lane_idx];
+                    if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
+                }
                 if (row_ok) {
                     a.row_max[(int64_t)s * R + r] = M * a.inv_scale;
                     a.row_sum[(int64_t)s * R + r] = S;
@@ -229,76 +226,62 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::named_bar_sync(1, kEpiWarps * 32);
         }
 
-        // ---- pass 2 (thread = key): column mass and below-threshold counts
-        //   u = l*c1 - mb_r ~ log2(exp(logit - max));  below <=> u < t* log2e;
-        //   mass = 2^(u - log2 S_r).  Serial over the CTA's rows: no cross-lane
-        //   reduction, and every key column follows the same summation order.
-        float* colp = a.col_partial + ((int64_t)s * nrb + rb) * a.n;
+        // ---- pass 2 (thread = key): column mass and below-threshold counts over
+        //   the 32 rows of group cg.  u = l*c1 - mb_r ~ log2(exp(logit - max));
+        //   below <=> u < t* log2e; mass = 2^(u - log2 S_r).  Serial per key: no
+        //   cross-lane reduction, and every key column follows the same order.
+        //   Each row group writes its own partial row of col_partial (no barrier).
+        const int r0 = cg * 32;
+        const int64_t rg = r_first + r0;
+        const bool one_head = rg / a.w == (rg + 31) / a.w;
+        float* colp = a.col_partial + ((int64_t)s * nparts + rb * 4 + cg) * a.n;
         for (int it = T; it < iters; ++it) {
             const int acc = it & 1;
             const int t = it - T;
-            const int p = t & 1;
             const int j = t * kN + lane_idx;                     // this thread's key
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
             sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
             sm100::tc_fence_after();
-            float colsum = 0.f;
-            int kcnt = 0;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int r0 = half * 64 + c * 32;
-                sm100::tmem_ld32(lane_addr + acc * kN + r0, l);
-                float csum = 0.f;
-                int cnt = 0;
-                if (all_visible) {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                        cnt += u < c_t2[r0 + k] ? 1 : 0;
-                        csum += ex2(u - c_ls[r0 + k]);
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const bool vis = j <= c_lim[r0 + k];
-                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                        cnt += (vis && u < c_t2[r0 + k]) ? 1 : 0;
-                        csum += vis ? ex2(u - c_ls[r0 + k]) : 0.f;
-                    }
-                }
-                colsum += csum;
-                kcnt += cnt;
-                // per-head totals (warp reduce, one shared atomic per warp)
-                const int64_t rg = r_first + r0;
-                if (rg / a.w == (rg + 31) / a.w) {
-                    const int tot = __reduce_add_sync(kFull, cnt);
-                    if (lane == 0 && tot) atomicAdd(hcnt + (int)(rg / a.w - head0), tot);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const bool vis = all_visible || j <= c_lim[r0 + k];
-                        const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                        const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k]) ? 1 : 0);
-                        if (lane == 0 && tot) atomicAdd(hcnt + (int)((rg + k) / a.w - head0), tot);
-                    }
-                }
-            }
+            sm100::tmem_ld32(lane_addr + acc * kN, l);
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + acc);
-            colbuf[(p * 2 + half) * kN + lane_idx] = colsum;
-            if (a.below_col) kcntbuf[(p * 2 + half) * kN + lane_idx] = kcnt;
-            sm100::named_bar_sync(1, kEpiWarps * 32);
-            if (half == 0 && j < a.n) {
-                colp[j] = colbuf[(p * 2) * kN + lane_idx] + colbuf[(p * 2 + 1) * kN + lane_idx];
-                if (a.below_col) {
-                    const int kc = kcntbuf[(p * 2) * kN + lane_idx] + kcntbuf[(p * 2 + 1) * kN + lane_idx];
-                    if (kc) atomicAdd(a.below_col + (int64_t)s * a.n + j, kc);
+            float csum = 0.f;
+            int cnt = 0;
+            if (all_visible) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                    cnt += u < c_t2[r0 + k] ? 1 : 0;
+                    csum += ex2(u - c_ls[r0 + k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const bool vis = j <= c_lim[r0 + k];
+                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                    cnt += (vis && u < c_t2[r0 + k]) ? 1 : 0;
+                    csum += vis ? ex2(u - c_ls[r0 + k]) : 0.f;
+                }
+            }
+            if (j < a.n) colp[j] = csum;
+            if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
+            // per-head totals (warp reduce, one shared atomic per warp)
+            if (one_head) {
+                const int tot = __reduce_add_sync(kFull, cnt);
+                if (lane == 0 && tot) atomicAdd(hcnt + (int)(rg / a.w - head0), tot);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {
+                    const bool vis = all_visible || j <= c_lim[r0 + k];
+                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k]) ? 1 : 0);
+                    if (lane == 0 && tot) atomicAdd(hcnt + (int)((rg + k) / a.w - head0), tot);
                 }
             }
         }
         // columns no row of this block can see
-        for (int64_t jj = (int64_t)T * kN + (ew * 32 + lane); jj < a.n; jj += kEpiWarps * 32) colp[jj] = 0.f;
+        for (int64_t jj = (int64_t)T * kN + lane_idx; jj < a.n; jj += kN) colp[jj] = 0.f;
         sm100::named_bar_sync(1, kEpiWarps * 32);
         const int nheads = (int)(r_last / a.w - head0 + 1);
         for (int h = ew * 32 + lane; h < nheads; h += kEpiWarps * 32)
@@ -314,7 +297,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 
 // ---------------------------------------------------------------- host side
 template <int D>
-cudaError_t launch_tc(const ScoreArgs& a, int nrb, cudaStream_t st) {
+cudaError_t launch_tc(const ScoreArgs& a, int nparts, cudaStream_t st) {
     CUtensorMap qmap, kmap;
     const int64_t R = (int64_t)a.G * a.w;
     if (!make_tmap_2d(&qmap, a.q, (int64_t)a.slots * R, a.d, kM)) return cudaErrorInvalidValue;
@@ -322,16 +305,16 @@ cudaError_t launch_tc(const ScoreArgs& a, int nrb, cudaStream_t st) {
     const size_t sm = Layout<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid(nrb, a.slots);
-    score_stats_tc<D><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nrb);
+    dim3 grid(nparts / 4, a.slots);
+    score_stats_tc<D><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nparts);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_score_stats_tc(const ScoreArgs& a, int nrb, cudaStream_t st) {
-    if (a.d == 64) return launch_tc<64>(a, nrb, st);
-    if (a.d == 128) return launch_tc<128>(a, nrb, st);
+cudaError_t launch_score_stats_tc(const ScoreArgs& a, int nparts, cudaStream_t st) {
+    if (a.d == 64) return launch_tc<64>(a, nparts, st);
+    if (a.d == 128) return launch_tc<128>(a, nparts, st);
     return cudaErrorInvalidValue;
 }
 

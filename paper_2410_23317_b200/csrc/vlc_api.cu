@@ -69,7 +69,7 @@ const char* vlc_last_error(void) { return g_err; }
 
 float vlc_threshold_logit(double p) { return threshold_logit(p); }
 
-int64_t vlc_score_row_blocks(int64_t rows) { return vlc::score_row_blocks(rows); }
+int64_t vlc_score_partials(int64_t rows) { return vlc::score_partials(rows); }
 
 int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t group,
                     int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
@@ -171,7 +171,7 @@ int vlc_select(const float* col_partial, const double* scores_in, int32_t slots,
         return fail(VLC_EINVAL, "select: n_keys > 24576 needs key_scratch");
     vlc::SelectArgs a{};
     a.col_partial = col_partial; a.slots = slots;
-    a.nrb = (int)vlc::score_row_blocks((int64_t)group * window);
+    a.nrb = (int)vlc::score_partials((int64_t)group * window);
     a.Hkv = kv_heads; a.L = layers; a.G = group; a.n = n_keys;
     a.kept_counts = kept_counts; a.kept_off = kept_off; a.recent_frac = recent_frac;
     a.kept_idx = kept_idx; a.kept_slot = kept_slot; a.scores = scores_out; a.scores_in = scores_in;

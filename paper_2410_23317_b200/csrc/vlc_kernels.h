@@ -26,13 +26,13 @@ struct ScoreArgs {
     float inv_scale, t_star;
     float* row_max;                    // [slots*R]
     float* row_sum;                    // [slots*R]
-    float* col_partial;                // [slots, nrb, n]  per row-block column sums
+    float* col_partial;                // [slots, score_partials(G*w), n] column sums per 32-row group
     unsigned long long* below_head;    // [slots*G]  (zeroed by the launcher)
     int* below_col;                    // optional [slots, n] (zeroed by the launcher)
 };
-int score_row_blocks(int64_t rows);  // nrb for R rows
+int score_partials(int64_t rows);    // col_partial rows per slot for R window rows
 cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st);
-cudaError_t launch_score_stats_tc(const ScoreArgs& a, int nrb, cudaStream_t st);  // head_dim 64 / 128
+cudaError_t launch_score_stats_tc(const ScoreArgs& a, int nparts, cudaStream_t st);  // head_dim 64 / 128
 
 // K2: numpy-exact gamma -> gamma' -> beta -> kept counts, plus ragged offsets.
 struct BudgetArgs {
@@ -56,7 +56,7 @@ cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st);
 
 // K3: per-slot top-k with recent reserve -> ascending kept indices.
 struct SelectArgs {
-    const float* col_partial;  // [slots, nrb, n]
+    const float* col_partial;  // [slots, nrb, n]  (nrb = score_partials rows)
     int slots, nrb, Hkv, L, G;
     int64_t n;                 // prompt_len m
     const int64_t* kept_counts;  // [B, L]

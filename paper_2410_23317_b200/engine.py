@@ -26,7 +26,7 @@ from dataclasses import dataclass
 from . import _lib
 from .errors import DegenerateSparsityError, ValidationError
 
-_ROW_BLOCK = 128  # K1 rows per CTA; col_partial has ceil(G*w/128) blocks per slot
+_ROW_BLOCK = 128  # K1 rows per CTA; col_partial has 4 partials (32-row groups) per block
 
 
 def _ptr(t) -> int:
@@ -75,7 +75,8 @@ class Shape:
 
     @property
     def nrb(self) -> int:
-        return (self.G * self.w + _ROW_BLOCK - 1) // _ROW_BLOCK
+        """col_partial rows per slot (vlc_score_partials)."""
+        return 4 * ((self.G * self.w + _ROW_BLOCK - 1) // _ROW_BLOCK)
 
     @property
     def causal_per_head(self) -> int:
