@@ -248,12 +248,21 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             if (lane == 0) sm100::mbar_arrive(tempty + acc);
             float csum = 0.f;
             int cnt = 0;
+            const float4* mb4 = reinterpret_cast<const float4*>(c_mb + r0);
+            const float4* ls4 = reinterpret_cast<const float4*>(c_ls + r0);
+            const float4* t24 = reinterpret_cast<const float4*>(c_t2 + r0);
             if (all_visible) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    cnt += u < c_t2[r0 + k] ? 1 : 0;
-                    csum += ex2(u - c_ls[r0 + k]);
+                for (int q4 = 0; q4 < 8; ++q4) {
+                    const float4 mb = mb4[q4], ls = ls4[q4], t2 = t24[q4];
+                    const float mbv[4] = {mb.x, mb.y, mb.z, mb.w}, lsv[4] = {ls.x, ls.y, ls.z, ls.w};
+                    const float t2v[4] = {t2.x, t2.y, t2.z, t2.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
+                        cnt += u < t2v[e] ? 1 : 0;
+                        csum += ex2(u - lsv[e]);
+                    }
                 }
             } else {
 #pragma unroll
