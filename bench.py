@@ -52,6 +52,21 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` ("K1" / "K5") from the newest committed
+    ncu --set full capture (profiles/r*_traffic.json, tools/ncu_traffic.py)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        data = json.load(f)
+    if kernel not in data:
+        return None, None
+    return data[kernel]["bytes"], os.path.relpath(files[-1], ROOT)
+
+
 def synth_inputs(batch, seed0, w):
     """bf16-rounded host arrays [B, L, H, rows, d] from the reference generator."""
     from paper_2410_23317_b200.trace import GenSpec, iter_layers, round_to_bf16, synthesize_values
@@ -300,14 +315,16 @@ def run_gpu_arm(args):
     k1_tflops = k1_flops(B) / (k1_ms / 1e3) / 1e12
     dec_ms = float(np.mean(dec))
     if dec_ms >= k1_ms:
+        traffic, tsrc = ncu_traffic("K5")
         roof = {"kernel": "K5 decode_step (cold L2, per launch)", "bound": "hbm", "achieved": k5_achieved,
-                "peak": hbm_peak, "unit": "GB/s", "frac": k5_achieved / hbm_peak, "traffic": None,
-                "peak_source": src, "bytes_per_launch": float(np.mean(k5_bytes)),
+                "peak": hbm_peak, "unit": "GB/s", "frac": k5_achieved / hbm_peak, "traffic": traffic,
+                "traffic_source": tsrc, "peak_source": src, "bytes_per_launch": float(np.mean(k5_bytes)),
                 "launch_us": float(np.mean(k5_ms)) * 1e3}
     else:
+        traffic, tsrc = ncu_traffic("K1")
         roof = {"kernel": "K1 score_stats", "bound": "tensor", "achieved": k1_tflops, "peak": tc_peak,
-                "unit": "TFLOP/s", "frac": k1_tflops / tc_peak, "traffic": None, "peak_source": src,
-                "flops_per_launch": k1_flops(B), "launch_us": k1_ms * 1e3}
+                "unit": "TFLOP/s", "frac": k1_tflops / tc_peak, "traffic": traffic, "traffic_source": tsrc,
+                "peak_source": src, "flops_per_launch": k1_flops(B), "launch_us": k1_ms * 1e3}
 
     # e2e through the public API with host buffers
     e2e_ms = []
