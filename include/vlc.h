@@ -134,14 +134,17 @@ VLC_API int vlc_gather(const void *keys, const void *values, int32_t slots, int3
  * [B*L*Hq, head_dim].  head_dim in {64, 128}, G <= 8; scale as in K1.
  * k_cache / v_cache: bf16 [cache_rows, head_dim], 16-byte aligned, rows that
  * no step has written yet must hold finite values (zero-initialise once).
- * No workspace; one CTA per slot.
+ * No workspace; one CTA per slot.  Launched with programmatic dependent
+ * launch: chained != 0 promises that the previous kernel on `stream` is this
+ * cache's step `step - 1`, letting the step prefetch every row but that
+ * step's append while the previous kernel drains (pass 0 otherwise).
  */
 VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, const void *v_new,
                     int64_t kv_stride, void *k_cache, void *v_cache, int64_t cache_rows,
                     const int64_t *cache_off,
                     const int64_t *base_len, int64_t step, int32_t batch, int32_t layers,
-                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float *out,
-                    void *stream);
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, int32_t chained,
+                    float *out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -92,7 +92,7 @@ def decode_step(q, keys, values):
     out = torch.empty((g, dp), dtype=torch.float32, device="cuda")
     _lib.call("vlc_decode_step", qd.data_ptr(), dp, kd[n - 1:].data_ptr(), vd[n - 1:].data_ptr(), dp,
               kc.data_ptr(), vc.data_ptr(), n, cache_off.data_ptr(), base_len.data_ptr(), 0, 1, 1, 1, g,
-              dp, 1.0 / math.sqrt(d), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+              dp, 1.0 / math.sqrt(d), 0, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
     return out[:, :d].cpu().numpy()
 
 

@@ -13,7 +13,7 @@ import os
 from .errors import KernelError, ValidationError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libvlc_b200.so")
+LIB_PATH = os.environ.get("VLC_LIB_PATH") or os.path.join(_PKG, "libvlc_b200.so")   # override: tuning runs
 
 VLC_OK, VLC_EINVAL, VLC_EUNSUPPORTED, VLC_ECUDA = 0, -1, -2, -3
 
@@ -39,7 +39,7 @@ _SIGNATURES = {
                                   _P, _P, _P]),
     "vlc_gather": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
     "vlc_decode_step": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _I32,
-                                       _I32, _I32, _I32, _I32, _F64, _P, _P]),
+                                       _I32, _I32, _I32, _I32, _F64, _I32, _P, _P]),
 }
 
 _lib = None

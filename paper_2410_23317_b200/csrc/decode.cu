@@ -28,7 +28,10 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
 constexpr int kChunk = 64;      // rows per ring stage (8 per warp)
-constexpr int kStages = 3;
+#ifndef VLC_DEC_STAGES
+#define VLC_DEC_STAGES 3
+#endif
+constexpr int kStages = VLC_DEC_STAGES;
 
 template <int D>
 struct Cfg {
@@ -110,8 +113,16 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             sm100::tma_load_2d(kdst + C::kTile + kb * C::kBox, &vmap, &bar[st], kb * 64, y);
         }
     };
-    if (tid == 0)
-        for (int c = 0; c < kStages && c < nchunks; ++c) issue(c);
+    // Programmatic dependent launch: everything up to griddepcontrol.wait may
+    // overlap the previous kernel.  When the caller guarantees that kernel is
+    // this cache's decode step `step - 1` (a.chained), rows written before it
+    // are final (that step waited for them), so only the chunk holding row
+    // k + step - 1 (its append) must wait; the others stream in right away.
+    // Without that guarantee (a.chained == 0) every load waits.
+    const int pend = a.chained ? (int)((n - 2) / kChunk) : 0;
+    if (tid == 0 && a.chained)
+        for (int c = 0; c < kStages && c < nchunks; ++c)
+            if (c != pend) issue(c);
 
     // Q as A fragments (rows = heads; rows >= G and 8..15 are zero), per 16-dim k-step
     const uint32_t* qw = reinterpret_cast<const uint32_t*>(a.q);
@@ -126,6 +137,15 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             qa[kk][0] = qa[kk][1] = 0u;
         }
     }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid == 0) {
+        if (a.chained) {
+            if (pend < kStages && pend < nchunks) issue(pend);
+        } else {
+            for (int c = 0; c < kStages && c < nchunks; ++c) issue(c);
+        }
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     float o[C::NT][4];
 #pragma unroll
     for (int t = 0; t < C::NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
@@ -234,8 +254,17 @@ cudaError_t launch_dg(const DecodeArgs& a, const CUtensorMap& km, const CUtensor
     cudaError_t e = cudaFuncSetAttribute(decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)C::kBytes);
     if (e != cudaSuccess) return e;
-    decode_kernel<D, G><<<a.slots, kThreads, C::kBytes, st>>>(km, vm, a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(a.slots);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, decode_kernel<D, G>, km, vm, a);
 }
 
 template <int D>

@@ -198,8 +198,8 @@ int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const vo
                     int64_t kv_stride, void* k_cache, void* v_cache, int64_t cache_rows,
                     const int64_t* cache_off,
                     const int64_t* base_len, int64_t step, int32_t batch, int32_t layers,
-                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, float* out,
-                    void* stream) {
+                    int32_t kv_heads, int32_t group, int32_t head_dim, double scale, int32_t chained,
+                    float* out, void* stream) {
     if (!q || !k_new || !v_new || !k_cache || !v_cache || !cache_off || !base_len || !out)
         return fail(VLC_EINVAL, "decode_step: null pointer");
     if ((reinterpret_cast<uintptr_t>(k_cache) | reinterpret_cast<uintptr_t>(v_cache) |
@@ -215,6 +215,7 @@ int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const vo
     a.q = q; a.q_stride = q_stride; a.k_new = k_new; a.v_new = v_new; a.kv_stride = kv_stride;
     a.k_cache = k_cache; a.v_cache = v_cache; a.cache_off = cache_off; a.base_len = base_len;
     a.cache_rows = cache_rows;
+    a.chained = (chained != 0 && step > 0) ? 1 : 0;
     if (cache_rows < 1) return fail(VLC_EINVAL, "decode_step: cache_rows must be >= 1");
     a.step = step; a.slots = batch * layers * kv_heads; a.Hkv = kv_heads; a.L = layers; a.G = group;
     a.d = head_dim; a.out = out;

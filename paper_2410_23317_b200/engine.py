@@ -218,9 +218,11 @@ class VLCache:
         return self
 
     # ------------------------------------------------------------ decode
-    def decode_step(self, q_dec, keys, values, step):
+    def decode_step(self, q_dec, keys, values, step, chained=False):
         """K5 for decode step `step`: appends keys/values row m+step of every
-        slot, attends the G query rows q_dec[..., step, :] of each KV head."""
+        slot, attends the G query rows q_dec[..., step, :] of each KV head.
+        chained=True promises the previous kernel on the stream is step-1
+        (lets the step prefetch under programmatic dependent launch)."""
         s = self.shape
         if not 0 <= step < self.decode_steps:
             raise ValidationError(f"step: must be in [0, {self.decode_steps}), got {step}")
@@ -231,8 +233,8 @@ class VLCache:
         _lib.call("vlc_decode_step", q_dec.data_ptr() + step * s.d * esz, n_dec * s.d,
                   keys.data_ptr() + (s.m + step) * s.d * esz, values.data_ptr() + (s.m + step) * s.d * esz,
                   T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), self.cache_rows, _ptr(self.cache_off),
-                  _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, _ptr(self.out),
-                  _stream())
+                  _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, int(bool(chained)),
+                  _ptr(self.out), _stream())
         return self.out
 
     def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None):
@@ -254,12 +256,12 @@ class VLCache:
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 for t in range(n):   # warm-up launch outside capture
-                    self.decode_step(q_dec, keys, values, t)
+                    self.decode_step(q_dec, keys, values, t, chained=t > 0)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for t in range(n):
-                    self.decode_step(q_dec, keys, values, t)
+                    self.decode_step(q_dec, keys, values, t, chained=t > 0)
             self._graphs[key] = g
         g.replay()
         return self.out
