@@ -40,11 +40,7 @@ struct Layout {
     static constexpr uint32_t kKRegion = kN * 128;          // bytes per K k-block
     static constexpr uint32_t kQBytes = KB * kQRegion;
     static constexpr uint32_t kKBytes = KB * kKRegion;      // one stage
-    static constexpr uint32_t kBarOff = kQBytes + kStages * kKBytes;
-    static constexpr uint32_t kRowOff = kBarOff + 256;               // float2 [4 column groups][kM]
-    static constexpr uint32_t kConstOff = kRowOff + 4 * kM * 8;      // mb, ls, t2 f32 + lim i32, [kM] each
-    static constexpr uint32_t kHcntOff = kConstOff + 4 * kM * 4;     // i32 [kM] head counters
-    static constexpr uint32_t kBytes = kHcntOff + kM * 4 + 1024;     // + alignment slack
+    static constexpr uint32_t kBytes = kQBytes + kStages * kKBytes + 1024;   // + alignment slack
 };
 
 VLC_DEV float max32(const float (&l)[32]) {
@@ -61,19 +57,15 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     using LY = Layout<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LY::kBarOff);
-    uint64_t* full = bars;                    // [kStages]
-    uint64_t* empty = bars + kStages;         // [kStages]
-    uint64_t* qfull = bars + 2 * kStages;     // [1]
-    uint64_t* tfull = qfull + 1;              // [2]
-    uint64_t* tempty = tfull + 2;             // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    float2* rowstat = reinterpret_cast<float2*>(smem + LY::kRowOff);
-    float* c_mb = reinterpret_cast<float*>(smem + LY::kConstOff);    // row max (raw dot) * c1
-    float* c_ls = c_mb + kM;                                          // log2(row sum)
-    float* c_t2 = c_ls + kM;                                          // threshold on u (-inf: no row)
-    int* c_lim = reinterpret_cast<int*>(c_t2 + kM);                   // last visible key (-1: no row)
-    int* hcnt = reinterpret_cast<int*>(smem + LY::kHcntOff);
+    // small state in static shared memory (plain LDS/STS, not generic accesses)
+    __shared__ uint64_t full[kStages], empty[kStages], qfull[1], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_slot[1];
+    __shared__ float2 rowstat[4 * kM];                  // (max, sum) per column group and row
+    __shared__ __align__(16) float c_mb[kM];            // row max (raw dot) * c1
+    __shared__ __align__(16) float c_ls[kM];            // log2(row sum)
+    __shared__ __align__(16) float c_t2[kM];            // threshold on u (-inf: no row)
+    __shared__ int c_lim[kM];                           // last visible key (-1: no row)
+    __shared__ int hcnt[kM];                            // below counts per head of the block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int s = blockIdx.y, rb = blockIdx.x;
