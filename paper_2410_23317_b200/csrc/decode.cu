@@ -29,7 +29,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
 constexpr int kChunk = 64;      // rows per ring stage (8 per warp)
 #ifndef VLC_DEC_STAGES
-#define VLC_DEC_STAGES 3
+#define VLC_DEC_STAGES 2
 #endif
 constexpr int kStages = VLC_DEC_STAGES;
 
