@@ -95,3 +95,98 @@ def test_stats_tiny_and_ragged(w, n, qb):
     np.testing.assert_allclose(got[2], ref[2], rtol=1e-5, atol=1e-12)
     np.testing.assert_array_equal(got[3], ref[3])
     np.testing.assert_array_equal(got[4], ref[4])
+
+
+def test_full_m7b_generator_trace_matches_oracle():
+    """BASELINE configs[1] in full: LLaVA-1.6-Mistral-7B shapes, 32 layers,
+    generator trace (bf16-in) -- counts, budgets, kept sets and 4 decode steps
+    against the oracle (threaded over (layer, head) like the reference allows)."""
+    import os
+
+    L, HQ, HKV, D, M, TAU, N = 32, 32, 8, 128, 2960, 64, 4
+    spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M,
+                   post_vision_len=TAU, decode_len=N, seed=0)
+    host, dv = make_inputs(spec, TAU)
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), decode_steps=N, keep_scores=True)
+    eng.compress(dv["q_win"], dv["keys"], dv["values"])
+    threads = len(os.sched_getaffinity(0))
+    ref = O.compression_pass(host[0]["q_win"], host[0]["keys"], M, HQ // HKV, threads=threads)
+    ref_below = np.array([[ref["stats"][(l, h)][3].sum() for h in range(HQ)] for l in range(L)])
+    np.testing.assert_array_equal(eng.below_head.view(L, HQ).cpu().numpy(), ref_below)
+    np.testing.assert_array_equal(eng.gamma_mean.cpu().numpy(), ref["gamma_mean"])
+    np.testing.assert_array_equal(eng.kept_counts.cpu().numpy(), ref["kept_counts"])
+    kept = eng.kept_sets()[0]
+    check_kept_sets(kept, ref["kept"], ref["scores"], ref["kept_counts"])
+    outs = []
+    eng.decode(dv["q_dec"], dv["keys"], dv["values"], outputs=outs)
+    ref_out = O.decode_sequence(host[0]["q_dec"], host[0]["keys"], host[0]["values"], kept, M, HQ // HKV, N,
+                                layers=[0, 13, 31])
+    for s in range(N):
+        got = outs[s].view(L, HQ, D).cpu().numpy()
+        for l in (0, 13, 31):
+            np.testing.assert_allclose(got[l], ref_out[s][l], rtol=1e-4, atol=1e-5)
+
+
+def test_head_sharded_budgets_equal_unsharded():
+    """KV-head sharding (parallel.HeadShard): each 'rank' runs K1 on its KV
+    heads only; the zero-padded int64 counts summed over ranks (what the NCCL
+    all-reduce does) give bit-identical budgets and kept sets to one device."""
+    from paper_2410_23317_b200 import _lib
+    from paper_2410_23317_b200.parallel import HeadShard
+
+    L, HQ, HKV, D, M, TAU, WORLD = 2, 56, 8, 128, 1500, 64, 4
+    spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M,
+                   post_vision_len=TAU, decode_len=1, seed=9)
+    host, dv = make_inputs(spec, TAU)
+    full = VLCache(Shape(1, L, HQ, HKV, D, M, TAU))
+    full.compress(dv["q_win"], dv["keys"])
+    counts = torch.zeros((1, L, HQ), dtype=torch.int64, device="cuda")
+    locals_ = []
+    for r in range(WORLD):
+        sh = HeadShard(r, WORLD, HKV, HQ // HKV)
+        (klo, khi), (qlo, qhi) = sh.kv_range, sh.q_range
+        eng = VLCache(Shape(1, L, qhi - qlo, khi - klo, D, M, TAU), head_shard=sh)
+        eng.score_stats(dv["q_win"][:, :, qlo:qhi].contiguous(), dv["keys"][:, :, klo:khi].contiguous())
+        counts[:, :, qlo:qhi] += eng.below_head.view(1, L, qhi - qlo)
+        locals_.append((eng, klo, khi, qlo, qhi))
+    np.testing.assert_array_equal(counts.view(-1).cpu().numpy(), full.below_head.cpu().numpy())
+    for eng, klo, khi, qlo, qhi in locals_:
+        eng.below_alloc = counts.reshape(-1)
+        eng.allocate()
+        eng.select()
+        np.testing.assert_array_equal(eng.kept_counts.cpu().numpy(), full.kept_counts.cpu().numpy())
+        np.testing.assert_array_equal(eng.gamma_mean.cpu().numpy(), full.gamma_mean.cpu().numpy())
+        mine, ref = eng.kept_sets()[0], full.kept_sets()[0]
+        for l in range(L):
+            for kv in range(khi - klo):
+                np.testing.assert_array_equal(mine[l][kv], ref[l][klo + kv])
+
+
+@pytest.mark.parametrize("alpha", [0.01, 0.2, 1.0])
+def test_sweep_16k_context_properties(alpha):
+    """SWEEP shapes (16,384-token prompt) on 2 layers: budgets against the
+    oracle allocation of the device's own gamma', sorted kept sets with the
+    recent reserve, and decode against the oracle on one layer."""
+    import math
+
+    L, HQ, HKV, D, M, TAU = 2, 32, 8, 128, 16384, 64
+    spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M,
+                   post_vision_len=TAU, decode_len=2, seed=2)
+    host, dv = make_inputs(spec, TAU)
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), alpha=alpha, decode_steps=2, keep_scores=True)
+    eng.compress(dv["q_win"], dv["keys"], dv["values"])
+    gm = eng.gamma_mean.cpu().numpy()
+    _, _, kc = O.allocate_sparsity_aware(gm, alpha, M)
+    counts = eng.kept_counts.cpu().numpy()
+    np.testing.assert_array_equal(counts, kc)
+    sc = eng.scores.view(L, HKV, M).cpu().numpy()
+    kept = eng.kept_sets()[0]
+    for l in range(L):
+        for kv in range(HKV):
+            np.testing.assert_array_equal(kept[l][kv], O.evict(sc[l, kv], int(counts[l]), 0.1))
+    outs = []
+    eng.decode(dv["q_dec"], dv["keys"], dv["values"], outputs=outs)
+    ref_out = O.decode_sequence(host[0]["q_dec"], host[0]["keys"], host[0]["values"], kept, M, HQ // HKV, 2,
+                                layers=[1])
+    np.testing.assert_allclose(outs[1].view(L, HQ, D)[1].cpu().numpy(), ref_out[1][1], rtol=1e-4, atol=1e-5)
+    assert math.isclose(eng.beta_pre.sum().item(), alpha * L, rel_tol=1e-12)
