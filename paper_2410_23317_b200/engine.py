@@ -193,12 +193,15 @@ class VLCache:
                   self.max_rows, _ptr(self.k_cache), _ptr(self.v_cache), _stream())
 
     def _check_inputs_kv(self, keys, values):
+        """K4 reads only the kept rows, so keys / values may also be pinned host
+        tensors: the kernel then pulls just those rows over PCIe (zero-copy)."""
         s = self.shape
         import torch
 
         for name, t in (("keys", keys), ("values", values)):
-            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
-                raise ValidationError(f"{name}: must be a contiguous bf16 CUDA tensor")
+            host_ok = (not t.is_cuda) and t.is_pinned()
+            if t.dtype != torch.bfloat16 or not (t.is_cuda or host_ok) or not t.is_contiguous():
+                raise ValidationError(f"{name}: must be a contiguous bf16 CUDA or pinned host tensor")
             if t.dim() != 5 or tuple(t.shape[:3]) != (s.B, s.L, s.Hkv) or t.shape[4] != s.d:
                 raise ValidationError(f"{name}: expected [B, L, Hkv, T, d], got {tuple(t.shape)}")
 
@@ -218,26 +221,29 @@ class VLCache:
         return self
 
     # ------------------------------------------------------------ decode
-    def decode_step(self, q_dec, keys, values, step, chained=False):
-        """K5 for decode step `step`: appends keys/values row m+step of every
-        slot, attends the G query rows q_dec[..., step, :] of each KV head.
-        chained=True promises the previous kernel on the stream is step-1
-        (lets the step prefetch under programmatic dependent launch)."""
+    def decode_step(self, q_dec, keys, values, step, chained=False, row0=None):
+        """K5 for decode step `step`: appends row row0+step of keys / values
+        (row0 defaults to m: full [B, L, Hkv, T, d] tensors; pass row0=0 for
+        decode-row tensors [B, L, Hkv, n, d]) and attends the G query rows
+        q_dec[..., step, :] of each KV head.  chained=True promises the previous
+        kernel on the stream is step-1 (prefetch under programmatic dependent
+        launch)."""
         s = self.shape
         if not 0 <= step < self.decode_steps:
             raise ValidationError(f"step: must be in [0, {self.decode_steps}), got {step}")
         n_dec, T = q_dec.shape[3], keys.shape[3]
-        if step >= n_dec or s.m + step >= T:
+        r0 = s.m if row0 is None else int(row0)
+        if step >= n_dec or r0 + step >= T:
             raise ValidationError("step: beyond the provided decode rows")
         esz = 2
         _lib.call("vlc_decode_step", q_dec.data_ptr() + step * s.d * esz, n_dec * s.d,
-                  keys.data_ptr() + (s.m + step) * s.d * esz, values.data_ptr() + (s.m + step) * s.d * esz,
+                  keys.data_ptr() + (r0 + step) * s.d * esz, values.data_ptr() + (r0 + step) * s.d * esz,
                   T * s.d, _ptr(self.k_cache), _ptr(self.v_cache), self.cache_rows, _ptr(self.cache_off),
                   _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, int(bool(chained)),
                   _ptr(self.out), _stream())
         return self.out
 
-    def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None):
+    def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None, row0=None):
         """n_steps decode steps; with graph=True the launch sequence is captured
         once into a CUDA graph (per input pointers) and replayed."""
         import torch
@@ -245,26 +251,70 @@ class VLCache:
         n = self.decode_steps if n_steps is None else int(n_steps)
         if outputs is not None or not graph:
             for t in range(n):
-                self.decode_step(q_dec, keys, values, t)
+                self.decode_step(q_dec, keys, values, t, row0=row0)
                 if outputs is not None:
                     outputs.append(self.out.clone())
             return self.out
-        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), n)
+        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), n, row0)
         g = self._graphs.get(key)
         if g is None:
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 for t in range(n):   # warm-up launch outside capture
-                    self.decode_step(q_dec, keys, values, t, chained=t > 0)
+                    self.decode_step(q_dec, keys, values, t, chained=t > 0, row0=row0)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for t in range(n):
-                    self.decode_step(q_dec, keys, values, t, chained=t > 0)
+                    self.decode_step(q_dec, keys, values, t, chained=t > 0, row0=row0)
             self._graphs[key] = g
         g.replay()
         return self.out
+
+    # ------------------------------------------------------------ host entry
+    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec):
+        """End-to-end call with pinned HOST inputs (the reference API's setting:
+        traces live in host memory): copies Q windows, prompt keys, decode
+        queries and the decode steps' K/V rows to the device, compresses --
+        K4 pulls only the kept value rows straight from pinned host memory --
+        decodes every step, and returns (kept_counts, last decode output) on the
+        host.  Shapes: q_win [B,L,Hq,w,d], k/v_prompt [B,L,Hkv,m,d],
+        q_dec [B,L,Hq,n,d], k/v_dec [B,L,Hkv,n,d], bf16, pinned.
+        Returns (kept_counts, out, bytes copied host->device); the values pulled
+        zero-copy are zero_copy_bytes(kept_counts) once the stream has synced."""
+        import torch
+
+        s = self.shape
+        for name, t in (("q_win", q_win), ("k_prompt", k_prompt), ("v_prompt", v_prompt), ("q_dec", q_dec),
+                        ("k_dec", k_dec), ("v_dec", v_dec)):
+            if t.is_cuda or not t.is_pinned() or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                raise ValidationError(f"{name}: must be a contiguous pinned bf16 host tensor")
+        st = getattr(self, "_stage", None)
+        if st is None or st[0].shape != q_win.shape or st[1].shape != k_prompt.shape or st[2].shape != q_dec.shape:
+            st = (torch.empty_like(q_win, device="cuda"), torch.empty_like(k_prompt, device="cuda"),
+                  torch.empty_like(q_dec, device="cuda"), torch.empty_like(k_dec, device="cuda"),
+                  torch.empty_like(v_dec, device="cuda"),
+                  torch.empty(s.B * s.L, dtype=torch.int64).pin_memory(),
+                  torch.empty(self.out.numel(), dtype=torch.float32).pin_memory())
+            self._stage = st
+        d_qw, d_k, d_qd, d_kn, d_vn, h_counts, h_out = st
+        for dst, src in ((d_qw, q_win), (d_k, k_prompt), (d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
+            dst.copy_(src, non_blocking=True)
+        self.score_stats(d_qw, d_k)
+        self.allocate()
+        self.select()
+        self.gather(d_k, v_prompt)             # keys from the device copy, values zero-copy
+        self.decode(d_qd, d_kn, d_vn, row0=0)
+        h_counts.copy_(self.kept_counts, non_blocking=True)
+        h_out.copy_(self.out, non_blocking=True)
+        copied = sum(t.numel() * 2 for t in (q_win, k_prompt, q_dec, k_dec, v_dec))
+        return h_counts, h_out, copied
+
+    def zero_copy_bytes(self, host_counts) -> int:
+        """Value bytes K4 pulled from host memory: every kept row of every KV head."""
+        s = self.shape
+        return int(host_counts.sum().item()) * s.Hkv * s.d * 2
 
     # ------------------------------------------------------------ results
     def check(self):

@@ -190,3 +190,24 @@ def test_sweep_16k_context_properties(alpha):
                                 layers=[1])
     np.testing.assert_allclose(outs[1].view(L, HQ, D)[1].cpu().numpy(), ref_out[1][1], rtol=1e-4, atol=1e-5)
     assert math.isclose(eng.beta_pre.sum().item(), alpha * L, rel_tol=1e-12)
+
+
+def test_run_from_host_matches_device_path():
+    """The host-input entry point (pinned host tensors, values gathered
+    zero-copy over PCIe) gives the device path's budgets and outputs."""
+    L, HQ, HKV, D, M, TAU, N = 2, 8, 2, 128, 700, 32, 5
+    spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M,
+                   post_vision_len=TAU, decode_len=N, seed=12)
+    host, dv = make_inputs(spec, TAU)
+    ref = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), decode_steps=N)
+    ref.compress(dv["q_win"], dv["keys"], dv["values"])
+    out_ref = ref.decode(dv["q_dec"], dv["keys"], dv["values"]).clone()
+    pin = lambda t: t.cpu().contiguous().pin_memory()  # noqa: E731
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), decode_steps=N)
+    counts, out, copied = eng.run_from_host(
+        pin(dv["q_win"]), pin(dv["keys"][:, :, :, :M]), pin(dv["values"][:, :, :, :M]), pin(dv["q_dec"]),
+        pin(dv["keys"][:, :, :, M:M + N]), pin(dv["values"][:, :, :, M:M + N]))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(counts.numpy(), ref.kept_counts.cpu().numpy())
+    np.testing.assert_array_equal(out.numpy(), out_ref.cpu().numpy())
+    assert eng.zero_copy_bytes(counts) == int(counts.sum()) * HKV * D * 2
