@@ -7,13 +7,14 @@
 // One CTA per (b, l, kv) slot streams the slot's K and V rows through a
 // kStages-deep shared-memory ring of 64-row chunks, loaded by 2-D TMA with the
 // 128-byte swizzle so tensor-core fragments come out of shared memory
-// conflict-free.  The G <= 8 query heads of the KV head form the M rows of
-// mma.sync tiles (GQA: every key row is read from HBM once per step for the
-// whole group):
-//   S = Q K^T     m16n8k16, bf16 in, fp32 accumulate (exact products);
-//   O += P V      m16n8k8, P split into bf16 hi + lo parts (~2^-16 relative),
-//                 V exact bf16, fp32 accumulate.
-// Each of the 8 warps owns 8 rows of every chunk with its own online-softmax
+// conflict-free.  The G <= 8 query heads of the KV head are the N = 8 columns
+// of transposed mma.sync tiles (GQA: every key row is read from HBM once per
+// step for the whole group; no padding of the big M side):
+//   S^T = K Q^T    m16n8k16, M = 16 keys, bf16 in, fp32 accumulate (exact products);
+//   O^T += V^T P^T m16n8k16, M = 16 dims, K = 16 keys; P^T comes from the S^T
+//                  accumulator through movmatrix, split into bf16 hi + lo parts
+//                  (~2^-16 relative); V exact bf16, fp32 accumulate.
+// Each of the 4 warps owns 16 rows of every chunk with its own online-softmax
 // state; the warps' (max, sum, O) partials merge once at the end.  The chunk
 // holding row k + step takes it from k_new / v_new (patched into the swizzled
 // tile) and also appends it to the cache for later steps.
@@ -24,10 +25,10 @@
 namespace vlc {
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 4;
 constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
-constexpr int kChunk = 64;      // rows per ring stage (8 per warp)
+constexpr int kChunk = 64;      // rows per ring stage (16 per warp)
 #ifndef VLC_DEC_STAGES
 #define VLC_DEC_STAGES 2
 #endif
@@ -40,7 +41,7 @@ struct Cfg {
     static constexpr uint32_t kTile = KB * kBox;             // K (or V) tile of a chunk
     static constexpr uint32_t kStage = 2 * kTile;            // K + V
     static constexpr uint32_t kBytes = kStages * kStage + 1024;   // + alignment slack
-    static constexpr int NT = D / 8;                         // 8-dim output tiles
+    static constexpr int MT = D / 16;                        // 16-dim output tiles
 };
 
 // byte offset of 16-byte piece `c` (of the row's D/8) of row r inside a tile
@@ -57,20 +58,18 @@ VLC_DEV void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, 
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
 }
-// D = A(16x16, rows 8..15 zero) * B(16x8) + C, bf16 -> f32
-VLC_DEV void mma_k16(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+// D = A(16x16) * B(16x8) + C, bf16 -> f32, full A fragment
+VLC_DEV void mma16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// D = A(16x8, rows 8..15 zero) * B(8x8) + C
-VLC_DEV void mma_k8(float (&d)[4], uint32_t a0, uint32_t b0) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a0), "r"(0u), "r"(b0));
+VLC_DEV uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
 }
 VLC_DEV uint32_t pack_bf16(float lo, float hi) {
     uint32_t r;
@@ -80,16 +79,16 @@ VLC_DEV uint32_t pack_bf16(float lo, float hi) {
 VLC_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, DecodeArgs a) {
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar[kStages];
-    __shared__ float part_m[kWarps][kMaxG], part_s[kWarps][kMaxG];
+    __shared__ float part_m[kWarps][8], part_s[kWarps][8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int row = lane >> 2, quad = lane & 3;              // fragment row (query head), column pair
+    const int row = lane >> 2, quad = lane & 3;              // fragment row (key / dim), column pair (heads)
     const int s = blockIdx.x;
     const int64_t n = a.base_len[s / a.Hkv] + a.step + 1;    // rows this step
     const int64_t new_row = n - 1;
@@ -124,17 +123,17 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         for (int c = 0; c < kStages && c < nchunks; ++c)
             if (c != pend) issue(c);
 
-    // Q as A fragments (rows = heads; rows >= G and 8..15 are zero), per 16-dim k-step
+    // Q^T as B fragments per 16-dim k-step: b0 = Q[head row][dims 2q, 2q+1], b1 = dims + 8
     const uint32_t* qw = reinterpret_cast<const uint32_t*>(a.q);
-    uint32_t qa[D / 16][2];
+    uint32_t qb[D / 16][2];
 #pragma unroll
     for (int kk = 0; kk < D / 16; ++kk) {
         if (row < G) {
             const int64_t base = (((int64_t)s * G + row) * a.q_stride + kk * 16) / 2;
-            qa[kk][0] = qw[base + quad];
-            qa[kk][1] = qw[base + 4 + quad];
+            qb[kk][0] = qw[base + quad];
+            qb[kk][1] = qw[base + 4 + quad];
         } else {
-            qa[kk][0] = qa[kk][1] = 0u;
+            qb[kk][0] = qb[kk][1] = 0u;
         }
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -146,10 +145,12 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         }
     }
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    float o[C::NT][4];
+    // O^T accumulators: tile t covers dims 16t..16t+15; c0,c1 = (dim 16t+row, heads 2q, 2q+1),
+    // c2,c3 = (dim 16t+row+8, heads 2q, 2q+1)
+    float o[C::MT][4];
 #pragma unroll
-    for (int t = 0; t < C::NT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
-    float run_m = -INFINITY, run_s = 0.f;                    // head `row`, this thread's columns
+    for (int t = 0; t < C::MT; ++t) o[t][0] = o[t][1] = o[t][2] = o[t][3] = 0.f;
+    float run_m[2] = {-INFINITY, -INFINITY}, run_s[2] = {0.f, 0.f};   // heads 2q, 2q+1
     const float c1 = a.inv_scale * kLog2e;
 
     for (int c = 0; c < nchunks; ++c) {
@@ -171,64 +172,82 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             }
             __syncthreads();
         }
-        // ---- S = Q K^T for this warp's 8 rows (keys) of the chunk
-        const int kr = warp * 8;                               // first key of the warp
+        // ---- S^T = K Q^T for this warp's 16 keys
+        const int kr = warp * 16;                              // first key of the warp
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t kbase = sm100::smem_u32(ks);
+        const int arow = kr + (lane & 7) + ((lane >> 3) & 1) * 8;   // ldmatrix row of this lane
 #pragma unroll
-        for (int kk = 0; kk < D / 16; kk += 2) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(kbase + swz<D>(kr + (lane & 7), kk * 2 + (lane >> 3)), b0, b1, b2, b3);
-            mma_k16(sacc, qa[kk][0], qa[kk][1], b0, b1);
-            mma_k16(sacc, qa[kk + 1][0], qa[kk + 1][1], b2, b3);
+        for (int kk = 0; kk < D / 16; ++kk) {
+            uint32_t af[4];
+            ldsm_x4(kbase + swz<D>(arow, kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
+            mma16(sacc, af, qb[kk][0], qb[kk][1]);
         }
-        // ---- online softmax of head `row` over keys kr + 2*quad, +1
-        const int64_t jk = j0 + kr + 2 * quad;
-        const float l0 = jk < n ? sacc[0] : -INFINITY;
-        const float l1 = jk + 1 < n ? sacc[1] : -INFINITY;
-        float tm = fmaxf(l0, l1);
-        tm = fmaxf(tm, __shfl_xor_sync(kFull, tm, 1));
-        tm = fmaxf(tm, __shfl_xor_sync(kFull, tm, 2));
-        const float mn = fmaxf(run_m, tm);
-        const float mnb = mn == -INFINITY ? 0.f : mn * c1;    // rows of an empty tail chunk
-        const float p0 = ex2(fmaf(l0, c1, -mnb));
-        const float p1 = ex2(fmaf(l1, c1, -mnb));
-        if (__any_sync(kFull, mn != run_m)) {
-            const float sc = run_m == -INFINITY ? 0.f : ex2(fmaf(run_m, c1, -mnb));
+        // ---- online softmax per head over the warp's keys: thread holds keys
+        //      kr+row (c0, c1) and kr+row+8 (c2, c3) for heads 2q (c0, c2), 2q+1 (c1, c3)
+        const int64_t ja = j0 + kr + row, jb = ja + 8;
+        const float l00 = ja < n ? sacc[0] : -INFINITY, l01 = ja < n ? sacc[1] : -INFINITY;
+        const float l10 = jb < n ? sacc[2] : -INFINITY, l11 = jb < n ? sacc[3] : -INFINITY;
+        float tm0 = fmaxf(l00, l10), tm1 = fmaxf(l01, l11);
 #pragma unroll
-            for (int t = 0; t < C::NT; ++t) { o[t][0] *= sc; o[t][1] *= sc; }
-            run_s *= sc;
+        for (int o2 = 4; o2 < 32; o2 <<= 1) {
+            tm0 = fmaxf(tm0, __shfl_xor_sync(kFull, tm0, o2));
+            tm1 = fmaxf(tm1, __shfl_xor_sync(kFull, tm1, o2));
         }
-        run_m = mn;
-        run_s += p0 + p1;
-        // P as the A operand of m16n8k8: hi + lo bf16 parts
-        const float h0 = bf16_round(p0), h1 = bf16_round(p1);
-        const uint32_t phi = pack_bf16(h0, h1);
-        const uint32_t plo = pack_bf16(p0 - h0, p1 - h1);
-        // ---- O += P V over the warp's 8 keys, 8-dim output tiles
+        const float mn0 = fmaxf(run_m[0], tm0), mn1 = fmaxf(run_m[1], tm1);
+        const float mb0 = mn0 == -INFINITY ? 0.f : mn0 * c1, mb1 = mn1 == -INFINITY ? 0.f : mn1 * c1;
+        const float p00 = ex2(fmaf(l00, c1, -mb0)), p10 = ex2(fmaf(l10, c1, -mb0));
+        const float p01 = ex2(fmaf(l01, c1, -mb1)), p11 = ex2(fmaf(l11, c1, -mb1));
+        if (__any_sync(kFull, mn0 != run_m[0] || mn1 != run_m[1])) {
+            const float sc0 = run_m[0] == -INFINITY ? 0.f : ex2(fmaf(run_m[0], c1, -mb0));
+            const float sc1 = run_m[1] == -INFINITY ? 0.f : ex2(fmaf(run_m[1], c1, -mb1));
+#pragma unroll
+            for (int t = 0; t < C::MT; ++t) { o[t][0] *= sc0; o[t][1] *= sc1; o[t][2] *= sc0; o[t][3] *= sc1; }
+            run_s[0] *= sc0;
+            run_s[1] *= sc1;
+        }
+        run_m[0] = mn0;
+        run_m[1] = mn1;
+        run_s[0] += p00 + p10;
+        run_s[1] += p01 + p11;
+        // P^T as B fragments (keys x heads): transpose the two 8x8 key blocks;
+        // hi + lo bf16 parts
+        const float h00 = bf16_round(p00), h01 = bf16_round(p01), h10 = bf16_round(p10), h11 = bf16_round(p11);
+        const uint32_t bh0 = movmatrix_t(pack_bf16(h00, h01)), bh1 = movmatrix_t(pack_bf16(h10, h11));
+        const uint32_t bl0 = movmatrix_t(pack_bf16(p00 - h00, p01 - h01));
+        const uint32_t bl1 = movmatrix_t(pack_bf16(p10 - h10, p11 - h11));
+        // ---- O^T += V^T P^T: V^T A fragments by transposed ldmatrix of the warp's 16 rows
         const uint32_t vbase = sm100::smem_u32(vs);
+        const int vrow = kr + (lane & 7) + (lane >> 4) * 8;
 #pragma unroll
-        for (int t = 0; t < C::NT; t += 4) {
-            uint32_t v0, v1, v2, v3;
-            ldsm_x4_t(vbase + swz<D>(kr + (lane & 7), t + (lane >> 3)), v0, v1, v2, v3);
-            mma_k8(o[t], phi, v0);     mma_k8(o[t], plo, v0);
-            mma_k8(o[t + 1], phi, v1); mma_k8(o[t + 1], plo, v1);
-            mma_k8(o[t + 2], phi, v2); mma_k8(o[t + 2], plo, v2);
-            mma_k8(o[t + 3], phi, v3); mma_k8(o[t + 3], plo, v3);
+        for (int t = 0; t < C::MT; ++t) {
+            uint32_t af[4];
+            ldsm_x4_t(vbase + swz<D>(vrow, t * 2 + ((lane >> 3) & 1)), af[0], af[1], af[2], af[3]);
+            mma16(o[t], af, bh0, bh1);
+            mma16(o[t], af, bl0, bl1);
         }
         __syncthreads();                                       // stage consumed by every warp
         if (tid == 0 && c + kStages < nchunks) issue(c + kStages);
     }
 
-    // ---- merge the 8 warps: per head, (max, sum) then O, through shared memory
-    run_s += __shfl_xor_sync(kFull, run_s, 1);
-    run_s += __shfl_xor_sync(kFull, run_s, 2);
-    if (quad == 0 && row < G) { part_m[warp][row] = run_m; part_s[warp][row] = run_s; }
-    float* po = reinterpret_cast<float*>(smem);               // [kWarps][G][D], ring is idle now
-    if (row < G) {
+    // ---- merge the warps: per head, (max, sum) then O, through shared memory
 #pragma unroll
-        for (int t = 0; t < C::NT; ++t)
-            *reinterpret_cast<float2*>(po + (warp * G + row) * D + t * 8 + 2 * quad) = make_float2(o[t][0], o[t][1]);
+    for (int o2 = 4; o2 < 32; o2 <<= 1) {
+        run_s[0] += __shfl_xor_sync(kFull, run_s[0], o2);
+        run_s[1] += __shfl_xor_sync(kFull, run_s[1], o2);
+    }
+    if (row == 0) {
+        part_m[warp][2 * quad] = run_m[0]; part_s[warp][2 * quad] = run_s[0];
+        part_m[warp][2 * quad + 1] = run_m[1]; part_s[warp][2 * quad + 1] = run_s[1];
+    }
+    float* po = reinterpret_cast<float*>(smem);               // [kWarps][8 heads][D], ring is idle now
+#pragma unroll
+    for (int t = 0; t < C::MT; ++t) {
+        const int d0 = 16 * t + row;
+        po[(warp * 8 + 2 * quad) * D + d0] = o[t][0];
+        po[(warp * 8 + 2 * quad + 1) * D + d0] = o[t][1];
+        po[(warp * 8 + 2 * quad) * D + d0 + 8] = o[t][2];
+        po[(warp * 8 + 2 * quad + 1) * D + d0 + 8] = o[t][3];
     }
     __syncthreads();
     for (int idx = tid; idx < G * D; idx += kThreads) {
@@ -242,7 +261,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             if (part_m[w][g] == -INFINITY) continue;
             const float f = ex2((part_m[w][g] - M) * c1);
             S = fmaf(part_s[w][g], f, S);
-            O = fmaf(po[(w * G + g) * D + dim], f, O);
+            O = fmaf(po[(w * 8 + g) * D + dim], f, O);
         }
         a.out[((int64_t)s * G + g) * D + dim] = O / S;
     }
