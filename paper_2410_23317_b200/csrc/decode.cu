@@ -7,17 +7,21 @@
 // One CTA per (b, l, kv) slot streams the slot's K and V rows through a
 // kStages-deep shared-memory ring of 64-row chunks, loaded by 2-D TMA with the
 // 128-byte swizzle so tensor-core fragments come out of shared memory
-// conflict-free.  The G <= 8 query heads of the KV head are the N = 8 columns
-// of transposed mma.sync tiles (GQA: every key row is read from HBM once per
-// step for the whole group; no padding of the big M side):
+// conflict-free.  Two groups of four warps take alternate chunks (group c % 2
+// consumes chunk c), so two chunks are in compute at once and the serial
+// chain of the slot's longest-budget layers is halved; inside a group warp w
+// owns rows 16w .. 16w+15 of the chunk.  The G <= 8 query heads of the KV head
+// are the N = 8 columns of transposed mma.sync tiles (GQA: every key row is
+// read from HBM once per step for the whole group; no padding of the big M side):
 //   S^T = K Q^T    m16n8k16, M = 16 keys, bf16 in, fp32 accumulate (exact products);
 //   O^T += V^T P^T m16n8k16, M = 16 dims, K = 16 keys; P^T comes from the S^T
 //                  accumulator through movmatrix, split into bf16 hi + lo parts
 //                  (~2^-16 relative); V exact bf16, fp32 accumulate.
-// Each of the 4 warps owns 16 rows of every chunk with its own online-softmax
-// state; the warps' (max, sum, O) partials merge once at the end.  The chunk
-// holding row k + step takes it from k_new / v_new (patched into the swizzled
-// tile) and also appends it to the cache for later steps.
+// Each warp keeps its own online-softmax state; the eight warps' (max, sum, O)
+// partials merge once at the end.  A stage is refilled as soon as the four
+// warps that consumed it arrive on its "empty" barrier.  The chunk holding row
+// k + step takes it from k_new / v_new (patched into the swizzled tile) and
+// also appends it to the cache for later steps.
 #include "sm100.cuh"
 #include "vlc_common.cuh"
 #include "vlc_kernels.h"
@@ -25,12 +29,20 @@
 namespace vlc {
 namespace {
 
-constexpr int kWarps = 4;
+#ifndef VLC_DEC_GROUP_WARPS
+#define VLC_DEC_GROUP_WARPS 4
+#endif
+#ifndef VLC_DEC_GROUPS
+#define VLC_DEC_GROUPS 2
+#endif
+constexpr int kGroupWarps = VLC_DEC_GROUP_WARPS;   // warps per consumer group (16 rows each)
+constexpr int kGroups = VLC_DEC_GROUPS;            // groups take chunks round-robin
+constexpr int kWarps = kGroupWarps * kGroups;
 constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
-constexpr int kChunk = 64;      // rows per ring stage (16 per warp)
+constexpr int kChunk = 16 * kGroupWarps;        // rows per ring stage
 #ifndef VLC_DEC_STAGES
-#define VLC_DEC_STAGES 2
+#define VLC_DEC_STAGES 3
 #endif
 constexpr int kStages = VLC_DEC_STAGES;
 
@@ -79,15 +91,17 @@ VLC_DEV uint32_t pack_bf16(float lo, float hi) {
 VLC_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, 2)
 decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, DecodeArgs a) {
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar[kStages];
+    __shared__ uint64_t bar[kStages], empty[kStages];
+    __shared__ volatile int loaded[kStages];   // chunk last issued into each stage
     __shared__ float part_m[kWarps][8], part_s[kWarps][8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int grp = warp / kGroupWarps, wig = warp % kGroupWarps;   // consumer group, warp in group
     const int row = lane >> 2, quad = lane & 3;              // fragment row (key / dim), column pair (heads)
     const int s = blockIdx.x;
     const int64_t n = a.base_len[s / a.Hkv] + a.step + 1;    // rows this step
@@ -96,7 +110,11 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     const int nchunks = (int)((n + kChunk - 1) / kChunk);
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) sm100::mbar_init(&bar[i], 1);
+        for (int i = 0; i < kStages; ++i) {
+            sm100::mbar_init(&bar[i], 1);
+            sm100::mbar_init(&empty[i], kGroupWarps);
+            loaded[i] = -1;
+        }
         sm100::fence_barrier_init();
         sm100::tma_prefetch(&kmap);
         sm100::tma_prefetch(&vmap);
@@ -106,6 +124,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         const int st = c % kStages;
         uint8_t* kdst = smem + st * C::kStage;
         const int y = (int)(seg + (int64_t)c * kChunk);
+        loaded[st] = c;                                          // released by the arrive below
         sm100::mbar_expect_tx(&bar[st], C::kStage);
         for (int kb = 0; kb < C::KB; ++kb) {
             sm100::tma_load_2d(kdst + kb * C::kBox, &kmap, &bar[st], kb * 64, y);
@@ -153,27 +172,32 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     float run_m[2] = {-INFINITY, -INFINITY}, run_s[2] = {0.f, 0.f};   // heads 2q, 2q+1
     const float c1 = a.inv_scale * kLog2e;
 
-    for (int c = 0; c < nchunks; ++c) {
+    for (int c = grp; c < nchunks; c += kGroups) {
         const int st = c % kStages;
         const int64_t j0 = (int64_t)c * kChunk;
         uint8_t* ks = smem + st * C::kStage;
         uint8_t* vs = ks + C::kTile;
+        // A group can run a whole ring ahead of the other: wait until the
+        // stage has been re-issued for chunk c before waiting on its phase
+        // (a parity wait alone would also accept the stage's previous phase).
+        while (loaded[st] < c) { }
         sm100::mbar_wait(&bar[st], (c / kStages) & 1);
-        if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (CTA-uniform)
+        if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
             const int r = (int)(new_row - j0);
-            if (tid < 2 * (D / 8)) {
-                const bool isv = tid >= D / 8;
-                const int piece = tid % (D / 8);
+            const int gt = tid % (kGroupWarps * 32);
+            if (gt < 2 * (D / 8)) {
+                const bool isv = gt >= D / 8;
+                const int piece = gt % (D / 8);
                 const uint4 val = reinterpret_cast<const uint4*>(
                     static_cast<const __nv_bfloat16*>(isv ? a.v_new : a.k_new) + (int64_t)s * a.kv_stride)[piece];
                 *reinterpret_cast<uint4*>((isv ? vs : ks) + swz<D>(r, piece)) = val;
                 reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(isv ? a.v_cache : a.k_cache) +
                                          (seg + new_row) * D)[piece] = val;
             }
-            __syncthreads();
+            sm100::named_bar_sync(1 + grp, kGroupWarps * 32);
         }
         // ---- S^T = K Q^T for this warp's 16 keys
-        const int kr = warp * 16;                              // first key of the warp
+        const int kr = wig * 16;                               // first key of the warp
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t kbase = sm100::smem_u32(ks);
         const int arow = kr + (lane & 7) + ((lane >> 3) & 1) * 8;   // ldmatrix row of this lane
@@ -226,8 +250,13 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             mma16(o[t], af, bh0, bh1);
             mma16(o[t], af, bl0, bl1);
         }
-        __syncthreads();                                       // stage consumed by every warp
-        if (tid == 0 && c + kStages < nchunks) issue(c + kStages);
+        // stage consumed by this group's warps -> refill it (the group leader)
+        __syncwarp();
+        if (lane == 0) sm100::mbar_arrive(&empty[st]);
+        if (wig == 0 && lane == 0 && c + kStages < nchunks) {
+            sm100::mbar_wait(&empty[st], (c / kStages) & 1);
+            issue(c + kStages);
+        }
     }
 
     // ---- merge the warps: per head, (max, sum) then O, through shared memory
@@ -240,6 +269,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         part_m[warp][2 * quad] = run_m[0]; part_s[warp][2 * quad] = run_s[0];
         part_m[warp][2 * quad + 1] = run_m[1]; part_s[warp][2 * quad + 1] = run_s[1];
     }
+    __syncthreads();                                          // both groups are done with the ring
     float* po = reinterpret_cast<float*>(smem);               // [kWarps][8 heads][D], ring is idle now
 #pragma unroll
     for (int t = 0; t < C::MT; ++t) {

@@ -30,14 +30,19 @@ EncodeTiledFn encode_fn() {
 }  // namespace
 
 bool make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int d, int box_rows) {
+    return make_tmap_2d_strided(map, base, rows, d, d, box_rows, true);
+}
+
+bool make_tmap_2d_strided(CUtensorMap* map, const void* base, int64_t rows, int cols, int64_t row_stride,
+                          int box_rows, bool swizzle) {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return false;
-    cuuint64_t gdim[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-    cuuint64_t gstride[1] = {(cuuint64_t)d * 2};
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)row_stride * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
     cuuint32_t estride[2] = {1, 1};
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

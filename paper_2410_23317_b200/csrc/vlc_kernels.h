@@ -11,6 +11,10 @@ namespace vlc {
 // 2-D bf16 TMA map over [rows, d] (row-major): box = 64 elements (one 128-byte
 // swizzle row) x box_rows, SWIZZLE_128B.  False if the driver entry is missing.
 bool make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int d, int box_rows);
+// 2-D bf16 TMA map over `rows` rows of `cols` elements, `row_stride` elements
+// apart (multiple of 8): box = 64 x box_rows, SWIZZLE_128B or none.
+bool make_tmap_2d_strided(CUtensorMap* map, const void* base, int64_t rows, int cols, int64_t row_stride,
+                          int box_rows, bool swizzle);
 
 constexpr int kDecodeChunk = 32;   // keys per K5 bulk-copy stage
 constexpr int kDecodeCluster = 8;  // CTAs per (b, l, kv) slot in K5 (one cluster)
