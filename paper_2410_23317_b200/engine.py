@@ -179,6 +179,21 @@ class VLCache:
                   _ptr(self.gamma_mean), _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
                   _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.status), _stream())
 
+    def allocate_from_gamma(self, gamma_mean):
+        """K2 from a given head-mean sparsity gamma_mean (f64 CUDA [B, L]) instead of
+        K1's counts (reference budget.allocate_sparsity_aware on measured
+        sparsity, budget.py:86-111).  gamma_mean = 0 with alpha = 1 keeps every
+        token: the full-cache decode baseline on the same kernels."""
+        s = self.shape
+        import torch
+
+        if tuple(gamma_mean.shape) != (s.B, s.L) or gamma_mean.dtype != torch.float64 or not gamma_mean.is_cuda:
+            raise ValidationError(f"gamma_mean: expected a float64 CUDA tensor [{s.B}, {s.L}]")
+        self.gamma_mean.copy_(gamma_mean.reshape(-1))
+        _lib.call("vlc_allocate_from_gamma", _ptr(self.gamma_mean), s.B, s.L, s.Hkv, s.m, self.alpha, self.beta_min,
+                  self.beta_max, self.decode_steps, _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
+                  _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.status), _stream())
+
     def select(self):
         s = self.shape
         _lib.call("vlc_select", _ptr(self.col_partial), 0, s.slots, s.Hkv, s.L, s.G, s.m, s.w,
