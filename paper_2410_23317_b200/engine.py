@@ -288,16 +288,36 @@ class VLCache:
         return self.out
 
     # ------------------------------------------------------------ host entry
-    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec):
+    def score_stats_layers(self, q_win, keys, b, l0, l1):
+        """K1 over the slots of prompt b, layers [l0, l1) only (their outputs
+        land where score_stats would put them): lets the compression start on
+        the first layers while later ones are still in flight."""
+        s = self.shape
+        self._check_inputs(q_win, keys)
+        if not (0 <= b < s.B and 0 <= l0 < l1 <= s.L):
+            raise ValidationError(f"layers: need 0 <= l0 < l1 <= {s.L} and 0 <= b < {s.B}")
+        slot0 = (b * s.L + l0) * s.Hkv
+        R, esz = s.G * s.w, 2
+        T = keys.shape[3]
+        _lib.call("vlc_score_stats", q_win.data_ptr() + slot0 * R * s.d * esz, keys.data_ptr() + slot0 * T * s.d * esz,
+                  (l1 - l0) * s.Hkv, s.G, s.d, T, s.m, s.w, s.m - s.w, self.p, self.scale,
+                  _ptr(self.row_max) + slot0 * R * 4, _ptr(self.row_sum) + slot0 * R * 4,
+                  _ptr(self.col_partial) + slot0 * s.nrb * s.m * 4, _ptr(self.below_head) + slot0 * s.G * 8,
+                  0, _stream())
+
+    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4):
         """End-to-end call with pinned HOST inputs (the reference API's setting:
         traces live in host memory): copies Q windows, prompt keys, decode
         queries and the decode steps' K/V rows to the device, compresses --
         K4 pulls only the kept value rows straight from pinned host memory --
         decodes every step, and returns (kept_counts, last decode output) on the
-        host.  Shapes: q_win [B,L,Hq,w,d], k/v_prompt [B,L,Hkv,m,d],
-        q_dec [B,L,Hq,n,d], k/v_dec [B,L,Hkv,n,d], bf16, pinned.
-        Returns (kept_counts, out, bytes copied host->device); the values pulled
-        zero-copy are zero_copy_bytes(kept_counts) once the stream has synced."""
+        host.  The copies run on a side stream in `chunks` layer groups per
+        prompt and K1 starts on each group as soon as it has landed, so the
+        scoring hides under the PCIe transfer.  Shapes: q_win [B,L,Hq,w,d],
+        k/v_prompt [B,L,Hkv,m,d], q_dec [B,L,Hq,n,d], k/v_dec [B,L,Hkv,n,d],
+        bf16, pinned.  Returns (kept_counts, out, bytes copied host->device);
+        the values pulled zero-copy are zero_copy_bytes(kept_counts) once the
+        stream has synced."""
         import torch
 
         s = self.shape
@@ -313,13 +333,32 @@ class VLCache:
                   torch.empty(s.B * s.L, dtype=torch.int64).pin_memory(),
                   torch.empty(self.out.numel(), dtype=torch.float32).pin_memory())
             self._stage = st
+            self._copy_stream = torch.cuda.Stream()
         d_qw, d_k, d_qd, d_kn, d_vn, h_counts, h_out = st
-        for dst, src in ((d_qw, q_win), (d_k, k_prompt), (d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
-            dst.copy_(src, non_blocking=True)
-        self.score_stats(d_qw, d_k)
+        comp, cs = torch.cuda.current_stream(), self._copy_stream
+        cs.wait_stream(comp)                  # staging buffers free (previous call done with them)
+        per = -(-s.L // max(1, int(chunks)))
+        groups = []
+        with torch.cuda.stream(cs):
+            for b in range(s.B):
+                for l0 in range(0, s.L, per):
+                    l1 = min(s.L, l0 + per)
+                    d_qw[b, l0:l1].copy_(q_win[b, l0:l1], non_blocking=True)
+                    d_k[b, l0:l1].copy_(k_prompt[b, l0:l1], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    groups.append((b, l0, l1, ev))
+            for dst, src in ((d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
+                dst.copy_(src, non_blocking=True)
+            ev_dec = torch.cuda.Event()
+            ev_dec.record(cs)
+        for b, l0, l1, ev in groups:
+            comp.wait_event(ev)
+            self.score_stats_layers(d_qw, d_k, b, l0, l1)
         self.allocate()
         self.select()
         self.gather(d_k, v_prompt)             # keys from the device copy, values zero-copy
+        comp.wait_event(ev_dec)
         self.decode(d_qd, d_kn, d_vn, row0=0)
         h_counts.copy_(self.kept_counts, non_blocking=True)
         h_out.copy_(self.out, non_blocking=True)
