@@ -18,7 +18,10 @@
 //                  accumulator through movmatrix, split into bf16 hi + lo parts
 //                  (~2^-16 relative); V exact bf16, fp32 accumulate.
 // Each warp keeps its own online-softmax state; the eight warps' (max, sum, O)
-// partials merge once at the end.  A stage is refilled as soon as the four
+// partials merge once at the end.  Under programmatic dependent launch only
+// the chunk holding the previous step's append (and the global writes) wait
+// for the previous step: everything else is loaded and computed while it
+// drains.  A stage is refilled as soon as the four
 // warps that consumed it arrive on its "empty" barrier.  The chunk holding row
 // k + step takes it from k_new / v_new (patched into the swizzled tile) and
 // also appends it to the cache for later steps.
@@ -91,7 +94,7 @@ VLC_DEV uint32_t pack_bf16(float lo, float hi) {
 VLC_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 512 / kThreads)
 decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, DecodeArgs a) {
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];
@@ -131,14 +134,31 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             sm100::tma_load_2d(kdst + C::kTile + kb * C::kBox, &vmap, &bar[st], kb * 64, y);
         }
     };
-    // Programmatic dependent launch: everything up to griddepcontrol.wait may
-    // overlap the previous kernel.  When the caller guarantees that kernel is
-    // this cache's decode step `step - 1` (a.chained), rows written before it
-    // are final (that step waited for them), so only the chunk holding row
-    // k + step - 1 (its append) must wait; the others stream in right away.
-    // Without that guarantee (a.chained == 0) every load waits.
-    const int pend = a.chained ? (int)((n - 2) / kChunk) : 0;
-    if (tid == 0 && a.chained)
+    // Programmatic dependent launch.  When the caller guarantees that the
+    // previous kernel is this cache's decode step `step - 1` (a.chained), rows
+    // written before it are final (that step waited for them), so only the
+    // chunk holding row k + step - 1 (its append, chunk `pend`) has to wait
+    // for it: the TMA of that chunk is issued after griddepcontrol.wait, and
+    // every thread waits before its first global write (the append, the
+    // output).  All other chunks are loaded AND computed while the previous
+    // step drains.  The next step may launch once a thread of every CTA is
+    // past its wait (this step's predecessor is then complete, so all the next
+    // step reads early is final).  Without the guarantee (a.chained == 0)
+    // everything waits up front.
+    const int pend = a.chained ? (int)((n - 2) / kChunk) : -1;
+    bool waited = !a.chained;
+    auto wait_prev = [&]() {
+        if (!waited) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            waited = true;
+        }
+    };
+    if (!a.chained) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+    if (tid == 0)
         for (int c = 0; c < kStages && c < nchunks; ++c)
             if (c != pend) issue(c);
 
@@ -155,15 +175,10 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             qb[kk][0] = qb[kk][1] = 0u;
         }
     }
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tid == 0) {
-        if (a.chained) {
-            if (pend < kStages && pend < nchunks) issue(pend);
-        } else {
-            for (int c = 0; c < kStages && c < nchunks; ++c) issue(c);
-        }
+    if (tid == 0 && pend >= 0 && pend < kStages && pend < nchunks) {   // an initial chunk waits
+        wait_prev();
+        issue(pend);
     }
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // O^T accumulators: tile t covers dims 16t..16t+15; c0,c1 = (dim 16t+row, heads 2q, 2q+1),
     // c2,c3 = (dim 16t+row+8, heads 2q, 2q+1)
     float o[C::MT][4];
@@ -183,6 +198,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         while (loaded[st] < c) { }
         sm100::mbar_wait(&bar[st], (c / kStages) & 1);
         if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
+            wait_prev();                                           // the append is a global write
             const int r = (int)(new_row - j0);
             const int gt = tid % (kGroupWarps * 32);
             if (gt < 2 * (D / 8)) {
@@ -255,10 +271,12 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         if (lane == 0) sm100::mbar_arrive(&empty[st]);
         if (wig == 0 && lane == 0 && c + kStages < nchunks) {
             sm100::mbar_wait(&empty[st], (c / kStages) & 1);
+            if (c + kStages == pend) wait_prev();             // holds the previous step's append
             issue(c + kStages);
         }
     }
 
+    wait_prev();                                              // before the output writes
     // ---- merge the warps: per head, (max, sum) then O, through shared memory
 #pragma unroll
     for (int o2 = 4; o2 < 32; o2 <<= 1) {
