@@ -276,3 +276,24 @@ def test_evict_api_matches_reference_including_ties(golden):
     assert vl.top_k_indices(np.array([3.0, 1.0, 3.0, 2.0]), 2).tolist() == [0, 2]
     assert vl.top_k_indices(np.zeros(5), 3).tolist() == [2, 3, 4]
     assert vl.top_k_indices(np.array([-0.0, 0.0, -1.0]), 1).tolist() == [1]
+
+
+def test_fixed_budgets_through_compress_cache(golden):
+    """Uniform / pyramid budgets (reference budget.py:114-147) drive K3 through
+    the library path; kept sets against the oracle's evict on the reference's
+    own TOY scores."""
+    import paper_2410_23317_b200 as vl
+    from paper_2410_23317_b200.trace import AttentionTrace, generate_trace
+
+    spec = GenSpec(**{**TOY, "num_kv_heads": 2})
+    tr, _ = generate_trace(spec)
+    tr = AttentionTrace(tr.header, tr.layout, [bf16(x) for x in tr.queries], [bf16(x) for x in tr.keys])
+    m, L = tr.header.prompt_len, tr.header.num_layers
+    scores = golden["toy2_scores"]
+    for alloc in (vl.allocate_uniform(0.1, L, m), vl.allocate_pyramid(0.1, L, m, decay_ratio=0.5),
+                  vl.allocate_pyramid(0.05, L, m, decay_ratio=0.2)):
+        res = vl.compress_cache(tr, alloc, vl.PostVision())
+        got = [[ks.kept for ks in row] for row in res.kept_sets]
+        ref = [[O.evict(scores[l, kv], int(alloc.kept_counts[l])) for kv in range(scores.shape[1])]
+               for l in range(L)]
+        check_kept_sets(got, ref, scores, alloc.kept_counts)
