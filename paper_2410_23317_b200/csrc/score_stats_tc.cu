@@ -62,7 +62,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ uint32_t tmem_slot[1];
     __shared__ float2 rowstat[4 * kM];                  // (max, sum) per column group and row
     __shared__ __align__(16) float c_mb[kM];            // row max (raw dot) * c1
-    __shared__ __align__(16) float c_ls[kM];            // log2(row sum)
+    __shared__ __align__(16) float c_is[kM];            // 1 / row sum (0: no row)
     __shared__ __align__(16) float c_t2[kM];            // threshold on u (-inf: no row)
     __shared__ int c_lim[kM];                           // last visible key (-1: no row)
     __shared__ int hcnt[kM];                            // below counts per head of the block
@@ -205,12 +205,12 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     a.row_max[(int64_t)s * R + r] = M * a.inv_scale;
                     a.row_sum[(int64_t)s * R + r] = S;
                     c_mb[lane_idx] = M * c1;
-                    c_ls[lane_idx] = __log2f(S);
+                    c_is[lane_idx] = 1.f / S;
                     c_t2[lane_idx] = a.t_star * kLog2e;
                     c_lim[lane_idx] = (int)(a.q_base + i);
                 } else {
                     c_mb[lane_idx] = INFINITY;    // u = -inf: no mass
-                    c_ls[lane_idx] = 0.f;
+                    c_is[lane_idx] = 0.f;
                     c_t2[lane_idx] = -INFINITY;   // never below
                     c_lim[lane_idx] = -1;         // sees no key
                 }
@@ -238,33 +238,36 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::tc_fence_before();
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + acc);
-            float csum = 0.f;
-            int cnt = 0;
+            // per entry: u = l*c1 - mb_r (log2 of exp(logit - max)), below <=> u < t2_r,
+            // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
+            // as a float (set + add).  The same operation order in every branch,
+            // so identical key columns give bit-identical mass.
+            float csum = 0.f, cntf = 0.f;
             const float4* mb4 = reinterpret_cast<const float4*>(c_mb + r0);
-            const float4* ls4 = reinterpret_cast<const float4*>(c_ls + r0);
-            const float4* t24 = reinterpret_cast<const float4*>(c_t2 + r0);
-            if (all_visible) {
+            const float4* is4 = reinterpret_cast<const float4*>(c_is + r0);
+            if (all_visible && r_first + r0 + 31 < R) {   // every row real and every key visible
+                const float t2c = a.t_star * kLog2e;
 #pragma unroll
                 for (int q4 = 0; q4 < 8; ++q4) {
-                    const float4 mb = mb4[q4], ls = ls4[q4], t2 = t24[q4];
-                    const float mbv[4] = {mb.x, mb.y, mb.z, mb.w}, lsv[4] = {ls.x, ls.y, ls.z, ls.w};
-                    const float t2v[4] = {t2.x, t2.y, t2.z, t2.w};
+                    const float4 mb = mb4[q4], iv = is4[q4];
+                    const float mbv[4] = {mb.x, mb.y, mb.z, mb.w}, ivv[4] = {iv.x, iv.y, iv.z, iv.w};
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
-                        cnt += u < t2v[e] ? 1 : 0;
-                        csum += ex2(u - lsv[e]);
+                        cntf += u < t2c ? 1.f : 0.f;
+                        csum = fmaf(ex2(u), ivv[e], csum);
                     }
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < 32; ++k) {
-                    const bool vis = j <= c_lim[r0 + k];
+                    const bool vis = all_visible || j <= c_lim[r0 + k];
                     const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    cnt += (vis && u < c_t2[r0 + k]) ? 1 : 0;
-                    csum += vis ? ex2(u - c_ls[r0 + k]) : 0.f;
+                    cntf += (vis && u < c_t2[r0 + k]) ? 1.f : 0.f;
+                    csum = vis ? fmaf(ex2(u), c_is[r0 + k], csum) : csum;
                 }
             }
+            const int cnt = (int)cntf;
             if (j < a.n) colp[j] = csum;
             if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
             // per-head totals (warp reduce, one shared atomic per warp)
