@@ -94,7 +94,10 @@ VLC_DEV uint32_t pack_bf16(float lo, float hi) {
 VLC_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 template <int D, int G>
-__global__ void __launch_bounds__(kThreads, 512 / kThreads)
+#ifndef VLC_DEC_MINB
+#define VLC_DEC_MINB (512 / kThreads)
+#endif
+__global__ void __launch_bounds__(kThreads, VLC_DEC_MINB)
 decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap, DecodeArgs a) {
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];

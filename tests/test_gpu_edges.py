@@ -211,3 +211,28 @@ def test_run_from_host_matches_device_path():
     np.testing.assert_array_equal(counts.numpy(), ref.kept_counts.cpu().numpy())
     np.testing.assert_array_equal(out.numpy(), out_ref.cpu().numpy())
     assert eng.zero_copy_bytes(counts) == int(counts.sum()) * HKV * D * 2
+
+
+def test_trace_file_to_run_from_host(tmp_path):
+    """A .vlct trace written to disk, read back memory-mapped and staged with
+    trace.engine_inputs drives run_from_host to the device path's results."""
+    from paper_2410_23317_b200.trace import engine_inputs, generate_trace, read_trace, write_trace
+
+    L, HQ, HKV, D, M, TAU, N = 2, 8, 2, 64, 300, 32, 3
+    spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M,
+                   post_vision_len=TAU, decode_len=N, seed=4)
+    tr, _ = generate_trace(spec)
+    write_trace(tr, tmp_path / "t.vlct")
+    back = read_trace(tmp_path / "t.vlct", mmap=True)
+    ins = engine_inputs(back, TAU)
+    ref = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), decode_steps=N)
+    dev = [t.cuda() for t in ins]
+    keys = torch.cat([dev[1], dev[4]], dim=3).contiguous()
+    vals = torch.cat([dev[2], dev[5]], dim=3).contiguous()
+    ref.compress(dev[0], keys, vals)
+    out_ref = ref.decode(dev[3], keys, vals).clone()
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), decode_steps=N)
+    counts, out, _ = eng.run_from_host(*ins)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(counts.numpy(), ref.kept_counts.cpu().numpy())
+    np.testing.assert_array_equal(out.numpy(), out_ref.cpu().numpy())
