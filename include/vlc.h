@@ -65,14 +65,22 @@ VLC_API int64_t vlc_score_partials(int64_t rows);
  *   below_head       : u64 [slots*G]  entries with exp(l - max) < p, per head
  *   below_col        : i32 [slots, n_keys] or NULL (per-column counts)
  * scale <= 0 selects 1/sqrt(head_dim) (zero-padded operands pass the true d's).
+ * exact_ws (NULL: off) -- exact mode: every below decision within a small
+ * band of flipping, and the near-max entries of every row, are re-decided
+ * from float64 dots exactly as the reference computes them, so below counts
+ * and row_max equal the reference's for bf16-representable inputs.
+ * exact_ws: 256-byte aligned, >= vlc_score_exact_bytes(slots, group, window,
+ * E) bytes for room for E listed entries (E >= slots*G*w is ample; beyond
+ * capacity the fp32 decision is kept).
  * Requires n_keys >= q_base + window, head_dim in {64, 128} (zero-pad smaller
  * dims and pass their scale), 16-byte aligned q_win / keys.
  */
+VLC_API int64_t vlc_score_exact_bytes(int32_t slots, int32_t group, int64_t window, int64_t entries);
 VLC_API int vlc_score_stats(const void *q_win, const void *keys, int32_t slots, int32_t group,
                     int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
                     int64_t q_base, double p, double scale, float *row_max, float *row_sum,
                     float *col_partial, uint64_t *below_head, int32_t *below_col,
-                    void *stream);
+                    void *exact_ws, int64_t exact_ws_bytes, void *stream);
 
 /*
  * K2 allocate.  gamma[b,l,h] = below/causal (reference sparsity.py:79),

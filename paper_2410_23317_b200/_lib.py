@@ -29,8 +29,9 @@ _SIGNATURES = {
     "vlc_last_error": (ctypes.c_char_p, []),
     "vlc_threshold_logit": (ctypes.c_float, [_F64]),
     "vlc_score_partials": (_I64, [_I64]),
+    "vlc_score_exact_bytes": (_I64, [_I32, _I32, _I64, _I64]),
     "vlc_score_stats": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64,
-                                       _F64, _P, _P, _P, _P, _P, _P]),
+                                       _F64, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "vlc_allocate": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64, _F64,
                                     _F64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vlc_allocate_from_gamma": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _F64, _F64, _F64, _I64,

@@ -50,7 +50,7 @@ VLC_DEV float max32(const float (&l)[32]) {
     return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
 }
 
-template <int D>
+template <int D, bool EXACT>
 __global__ void __launch_bounds__(kThreads, 1)
 score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                ScoreArgs a, int nparts) {
@@ -242,11 +242,15 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
             // as a float (set + add).  The same operation order in every branch,
             // so identical key columns give bit-identical mass.
-            float csum = 0.f, cntf = 0.f;
+            // exact mode: an entry whose decision u < t2 is within `band` of flipping
+            // (fp32 logits vs the reference's float64 dots) is not counted here but
+            // listed for a float64 re-decision.  band = 0: plain decisions.
+            const float band = EXACT ? a.band : 0.f;
+            float csum = 0.f, cntf = 0.f, cnth = 0.f;   // cnth - cntf: entries inside the band
             const float4* mb4 = reinterpret_cast<const float4*>(c_mb + r0);
             const float4* is4 = reinterpret_cast<const float4*>(c_is + r0);
             if (all_visible && r_first + r0 + 31 < R) {   // every row real and every key visible
-                const float t2c = a.t_star * kLog2e;
+                const float t2c = a.t_star * kLog2e, t2lo = t2c - band;
 #pragma unroll
                 for (int q4 = 0; q4 < 8; ++q4) {
                     const float4 mb = mb4[q4], iv = is4[q4];
@@ -254,7 +258,8 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
-                        cntf += u < t2c ? 1.f : 0.f;
+                        cntf += u < t2lo ? 1.f : 0.f;
+                        if (EXACT) cnth += u < t2c + band ? 1.f : 0.f;
                         csum = fmaf(ex2(u), ivv[e], csum);
                     }
                 }
@@ -263,11 +268,33 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 for (int k = 0; k < 32; ++k) {
                     const bool vis = all_visible || j <= c_lim[r0 + k];
                     const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    cntf += (vis && u < c_t2[r0 + k]) ? 1.f : 0.f;
+                    const float t2 = c_t2[r0 + k];
+                    cntf += (vis && u < t2 - band) ? 1.f : 0.f;
+                    if (EXACT) cnth += (vis && u < t2 + band) ? 1.f : 0.f;
                     csum = vis ? fmaf(ex2(u), c_is[r0 + k], csum) : csum;
                 }
             }
-            const int cnt = (int)cntf;
+            int cnt = (int)cntf;
+            if (EXACT && __any_sync(kFull, cnth != cntf)) {
+                // reserve this thread's entries with one atomic, then write them
+                const int nf = (int)(cnth - cntf);
+                int at = nf ? atomicAdd(a.fix_counts + 1, nf) : 0;
+#pragma unroll
+                for (int k = 0; k < 32; ++k) {   // static indices: l stays in registers
+                    const bool vis = j < a.n && (all_visible || j <= c_lim[r0 + k]);
+                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
+                    const float t2 = c_t2[r0 + k];
+                    if (nf && vis && u >= t2 - band && u < t2 + band) {
+                        if (at < a.cap) {
+                            a.flag[at] = make_int4(s, (int)(r_first + r0 + k), j, 1);
+                        } else {   // list full: keep the fp32 decision
+                            atomicAdd(a.fix_counts + 2, 1);
+                            cnt += u < t2 ? 1 : 0;
+                        }
+                        ++at;
+                    }
+                }
+            }
             if (j < a.n) colp[j] = csum;
             if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
             // per-head totals (warp reduce, one shared atomic per warp)
@@ -279,7 +306,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 for (int k = 0; k < 32; ++k) {
                     const bool vis = all_visible || j <= c_lim[r0 + k];
                     const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k]) ? 1 : 0);
+                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k] - band) ? 1 : 0);
                     if (lane == 0 && tot) atomicAdd(hcnt + (int)((rg + k) / a.w - head0), tot);
                 }
             }
@@ -300,18 +327,23 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 }
 
 // ---------------------------------------------------------------- host side
-template <int D>
-cudaError_t launch_tc(const ScoreArgs& a, int nparts, cudaStream_t st) {
+template <int D, bool EXACT>
+cudaError_t launch_tc_e(const ScoreArgs& a, int nparts, cudaStream_t st) {
     CUtensorMap qmap, kmap;
     const int64_t R = (int64_t)a.G * a.w;
     if (!make_tmap_2d(&qmap, a.q, (int64_t)a.slots * R, a.d, kM)) return cudaErrorInvalidValue;
     if (!make_tmap_2d(&kmap, a.k, (int64_t)a.slots * a.T, a.d, kN)) return cudaErrorInvalidValue;
     const size_t sm = Layout<D>::kBytes;
-    cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     dim3 grid(nparts / 4, a.slots);
-    score_stats_tc<D><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nparts);
+    score_stats_tc<D, EXACT><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nparts);
     return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_tc(const ScoreArgs& a, int nparts, cudaStream_t st) {
+    return a.cap > 0 ? launch_tc_e<D, true>(a, nparts, st) : launch_tc_e<D, false>(a, nparts, st);
 }
 
 }  // namespace

@@ -71,10 +71,16 @@ float vlc_threshold_logit(double p) { return threshold_logit(p); }
 
 int64_t vlc_score_partials(int64_t rows) { return vlc::score_partials(rows); }
 
+int64_t vlc_score_exact_bytes(int32_t slots, int32_t group, int64_t window, int64_t entries) {
+    if (slots < 1 || group < 1 || window < 1 || entries < 1) return -1;
+    return vlc::exact_ws_bytes(slots, (int64_t)group * window, entries);
+}
+
 int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t group,
                     int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
                     int64_t q_base, double p, double scale, float* row_max, float* row_sum, float* col_partial,
-                    uint64_t* below_head, int32_t* below_col, void* stream) {
+                    uint64_t* below_head, int32_t* below_col, void* exact_ws, int64_t exact_ws_bytes,
+                    void* stream) {
     if (!q_win || !keys || !row_max || !row_sum || !col_partial || !below_head)
         return fail(VLC_EINVAL, "score_stats: null pointer");
     if (slots < 1 || group < 1 || window < 1 || n_keys < 1 || q_base < 0)
@@ -96,6 +102,24 @@ int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t 
     a.row_max = row_max; a.row_sum = row_sum; a.col_partial = col_partial;
     a.below_head = reinterpret_cast<unsigned long long*>(below_head);
     a.below_col = below_col;
+    a.inv_scale_d = scale > 0.0 ? scale : 1.0 / std::sqrt((double)head_dim);
+    if (exact_ws) {
+        const int64_t rows = (int64_t)group * window;
+        const int cap = vlc::exact_ws_cap(exact_ws_bytes, slots, rows);
+        if (cap < 1 || (reinterpret_cast<uintptr_t>(exact_ws) & 255))
+            return fail(VLC_EINVAL, "score_stats: exact_ws must be 256-byte aligned and hold "
+                                    ">= vlc_score_exact_bytes(slots, group, window, 1) bytes");
+        uint8_t* ws = static_cast<uint8_t*>(exact_ws);
+        const int64_t rk = (slots * rows * 4 + 255) / 256 * 256;
+        a.fix_counts = reinterpret_cast<int*>(ws);
+        a.rmax_key = reinterpret_cast<unsigned*>(ws + 256);
+        a.rows = reinterpret_cast<int*>(ws + 256 + rk);
+        a.cand = reinterpret_cast<int4*>(ws + 256 + 2 * rk);
+        a.flag = a.cand + cap;
+        a.cap = cap;
+        a.band = 1.0f / 512.0f;   // log2 units: ~100x the fp32-accumulation error of a d <= 128 logit
+        a.err_max = a.band / 1.4426950408889634f / 16.0f;  // logit units (~10x the fp32 row-max error)
+    }
     return cuda_status(vlc::launch_score_stats(a, (cudaStream_t)stream), "score_stats");
 }
 

@@ -19,6 +19,11 @@ bool make_tmap_2d_strided(CUtensorMap* map, const void* base, int64_t rows, int 
 constexpr int kDecodeChunk = 32;   // keys per K5 bulk-copy stage
 constexpr int kDecodeCluster = 8;  // CTAs per (b, l, kv) slot in K5 (one cluster)
 
+// Exact-mode workspace of K1: [counts (256 B)] [rmax_key u32 slots*R] [rows
+// i32 slots*R] (each 256 B aligned) [cand int4 x cap] [flag int4 x cap].
+int64_t exact_ws_bytes(int64_t slots, int64_t rows, int64_t cap);
+int exact_ws_cap(int64_t bytes, int64_t slots, int64_t rows);    // <= 0: too small
+
 // K1: post-vision attention statistics for every (b, l, kv) slot.
 // Slot s = (b*L + l)*Hkv + kv owns window rows [s*R, s*R + R), R = G*w, i.e.
 // heads kv*G .. kv*G+G-1 of the [B, L, Hq, w, d] window tensor.
@@ -33,6 +38,18 @@ struct ScoreArgs {
     float* col_partial;                // [slots, score_partials(G*w), n] column sums per 32-row group
     unsigned long long* below_head;    // [slots*G]  (zeroed by the launcher)
     int* below_col;                    // optional [slots, n] (zeroed by the launcher)
+    // exact mode (fix != nullptr): entries whose below-threshold decision is
+    // within `band` (log2 units) of flipping, and the near-max entries that
+    // decide the row max, are listed and re-decided in float64 afterwards
+    int* fix_counts;                   // device [n_defer, n_flag, overflow, n_rows] (zeroed by the launcher)
+    unsigned* rmax_key;                // [slots*R] 1 = row listed, then key of its exact f32 max (0 = none)
+    int* rows;                         // [slots*R] rows whose exact max is needed
+    int4* cand;                        // [cap] (slot, row, key, mult) entries waiting for an exact row max
+    int4* flag;                        // [cap] (slot, row, key, mult) near-threshold entries
+    int cap;                           // 0: exact mode off
+    float band;                        // log2 units, K1's listing band
+    float err_max;                     // logit units: |fp32 row max - exact row max| bound
+    double inv_scale_d;                // the reference's 1/sqrt(d) (or scale) in double
 };
 int score_partials(int64_t rows);    // col_partial rows per slot for R window rows
 cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st);

@@ -95,7 +95,7 @@ class VLCache:
 
     def __init__(self, shape: Shape, *, alpha=0.1, p=0.01, recent_frac=0.10, beta_min=0.01,
                  beta_max=1.0, decode_steps=0, keep_scores=False, device=None, head_shard=None,
-                 scale=None):
+                 scale=None, exact=True):
         torch = _lib.require_cuda()
         if not 0.0 < alpha <= 1.0:
             raise ValidationError(f"alpha: must be in (0, 1], got {alpha}")
@@ -143,6 +143,9 @@ class VLCache:
         self.k_cache = torch.zeros(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.v_cache = torch.zeros(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty(s.B * s.L * s.Hq * s.d, dtype=f32, device=dev)
+        # K1 exact mode (vlc.h): room for one listed entry per window row and slot
+        self.exact_ws_bytes = int(_lib.load().vlc_score_exact_bytes(s.slots, s.G, s.w, max(1 << 16, s.slots * R)))
+        self.exact_ws = torch.empty(self.exact_ws_bytes, dtype=torch.uint8, device=dev) if exact else None
         self._graphs = {}
 
     # ------------------------------------------------------------ stages
@@ -169,7 +172,8 @@ class VLCache:
         self._check_inputs(q_win, keys)
         _lib.call("vlc_score_stats", q_win.data_ptr(), keys.data_ptr(), s.slots, s.G, s.d,
                   keys.shape[3], s.m, s.w, s.m - s.w, self.p, self.scale, _ptr(self.row_max), _ptr(self.row_sum),
-                  _ptr(self.col_partial), _ptr(self.below_head), _ptr(below_col), _stream())
+                  _ptr(self.col_partial), _ptr(self.below_head), _ptr(below_col), _ptr(self.exact_ws),
+                  self.exact_ws_bytes, _stream())
 
     def allocate(self):
         """K2 from the below-threshold counts currently in below_head."""
@@ -303,7 +307,7 @@ class VLCache:
                   (l1 - l0) * s.Hkv, s.G, s.d, T, s.m, s.w, s.m - s.w, self.p, self.scale,
                   _ptr(self.row_max) + slot0 * R * 4, _ptr(self.row_sum) + slot0 * R * 4,
                   _ptr(self.col_partial) + slot0 * s.nrb * s.m * 4, _ptr(self.below_head) + slot0 * s.G * 8,
-                  0, _stream())
+                  0, _ptr(self.exact_ws), self.exact_ws_bytes, _stream())
 
     def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4):
         """End-to-end call with pinned HOST inputs (the reference API's setting:

@@ -47,7 +47,7 @@ def test_score_stats_rejects_bad_p_before_cuda(p):
     lib = _lib.load()
     dummy = ctypes.c_void_p(16)
     rc = lib.vlc_score_stats(dummy, dummy, 1, 1, 64, 10, 10, 2, 8, p, 0.0, dummy, dummy, dummy, dummy,
-                             None, None)
+                             None, None, 0, None)
     assert rc == _lib.VLC_EINVAL
     assert b"p:" in lib.vlc_last_error()
     with pytest.raises(ValidationError, match="p:"):
@@ -63,10 +63,15 @@ def test_contract_errors_map_to_reference_types():
     assert rc == _lib.VLC_EINVAL and b"recent_window_frac" in lib.vlc_last_error()
     rc = lib.vlc_decode_step(d, 64, d, d, 64, d, d, 10, d, d, 0, 1, 1, 1, 9, 64, 0.0, 0, d, None)
     assert rc == _lib.VLC_EUNSUPPORTED
-    rc = lib.vlc_score_stats(d, d, 1, 1, 48, 10, 10, 2, 8, 0.01, 0.0, d, d, d, d, None, None)
+    rc = lib.vlc_score_stats(d, d, 1, 1, 48, 10, 10, 2, 8, 0.01, 0.0, d, d, d, d, None, None, 0, None)
     assert rc == _lib.VLC_EUNSUPPORTED   # head_dim not 64 / 128 (callers zero-pad)
-    rc = lib.vlc_score_stats(d, d, 1, 1, 64, 10, 9, 2, 8, 0.01, 0.0, d, d, d, d, None, None)
+    rc = lib.vlc_score_stats(d, d, 1, 1, 64, 10, 9, 2, 8, 0.01, 0.0, d, d, d, d, None, None, 0, None)
     assert rc == _lib.VLC_EINVAL         # n_keys < q_base + window
+    need = lib.vlc_score_exact_bytes(4, 2, 8, 100)
+    assert need > 0 and lib.vlc_score_exact_bytes(4, 2, 8, 0) < 0
+    ws = ctypes.c_void_p(256)
+    rc = lib.vlc_score_stats(d, d, 4, 2, 64, 10, 10, 8, 2, 0.01, 0.0, d, d, d, d, None, ws, 16, None)
+    assert rc == _lib.VLC_EINVAL and b"exact_ws" in lib.vlc_last_error()
 
 
 def test_compute_entry_points_fail_loudly_without_gpu():
