@@ -28,7 +28,18 @@ namespace {
 
 constexpr int kM = 128;          // window rows per CTA (UMMA M)
 constexpr int kN = 128;          // keys per tile (UMMA N)
-constexpr int kStages = 3;       // K tile ring
+#ifndef VLC_K1_STAGES
+#define VLC_K1_STAGES 3
+#endif
+#ifndef VLC_K1_SUB
+#define VLC_K1_SUB 32
+#endif
+#ifndef VLC_K1_MINB
+#define VLC_K1_MINB 1
+#endif
+constexpr int kStages = VLC_K1_STAGES;   // K tile ring
+constexpr int kSub = VLC_K1_SUB;         // TMEM columns an epilogue thread holds at a time (16 / 32)
+constexpr int kNSub = 32 / kSub;
 constexpr int kEpiWarps = 16;    // 4 per TMEM lane quarter, one 32-column group each
 constexpr int kThreads = 128 + kEpiWarps * 32;
 constexpr uint32_t kTmemCols = 2 * kN;
@@ -43,15 +54,26 @@ struct Layout {
     static constexpr uint32_t kBytes = kQBytes + kStages * kKBytes + 1024;   // + alignment slack
 };
 
-VLC_DEV float max32(const float (&l)[32]) {
-    float m[8];
+template <int N>
+VLC_DEV float maxn(const float (&l)[N]) {
+    float m[N / 4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) m[k] = fmaxf(fmaxf(l[4 * k], l[4 * k + 1]), fmaxf(l[4 * k + 2], l[4 * k + 3]));
-    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+    for (int k = 0; k < N / 4; ++k) m[k] = fmaxf(fmaxf(l[4 * k], l[4 * k + 1]), fmaxf(l[4 * k + 2], l[4 * k + 3]));
+#pragma unroll
+    for (int w = N / 8; w >= 1; w >>= 1)
+#pragma unroll
+        for (int k = 0; k < w; ++k) m[k] = fmaxf(m[k], m[k + w]);
+    return m[0];
+}
+
+template <int N>
+VLC_DEV void tmem_ld(uint32_t taddr, float (&v)[N]) {
+    if constexpr (N == 32) sm100::tmem_ld32(taddr, v);
+    else sm100::tmem_ld16(taddr, v);
 }
 
 template <int D, bool EXACT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, VLC_K1_MINB)
 score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
                ScoreArgs a, int nparts) {
     using LY = Layout<D>;
@@ -147,7 +169,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const int lane_idx = 32 * sub + lane;                  // TMEM lane of this thread
         const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + cg * 32;
         const float c1 = a.inv_scale * kLog2e;
-        float l[32];
+        float l[kSub];
 
         // ---- pass 1 (thread = window row): running max of raw dots, rescaled sum
         {
@@ -160,19 +182,23 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 const int acc = it & 1;
                 sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
                 sm100::tc_fence_after();
-                sm100::tmem_ld32(lane_addr + acc * kN, l);
-                sm100::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the chunk now
-                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
-                const bool full_chunk = __all_sync(kFull, valid == 32);
+#pragma unroll
+                for (int h = 0; h < kNSub; ++h) {
+                tmem_ld(lane_addr + acc * kN + h * kSub, l);
+                if (h == kNSub - 1) {
+                    sm100::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the chunk now
+                }
+                const int valid = (int)imax(0, imin(kSub, row_end - ((int64_t)it * kN + cg * 32 + h * kSub)));
+                const bool full_chunk = __all_sync(kFull, valid == kSub);
                 float cmax;
                 if (full_chunk) {
-                    cmax = max32(l);
+                    cmax = maxn(l);
                 } else {
                     cmax = -INFINITY;
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+                    for (int k = 0; k < kSub; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
                 }
                 if (cmax > m) {
                     sum *= ex2((m - cmax) * c1);   // 0 while m == -inf
@@ -182,12 +208,13 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 float acc_s = 0.f;
                 if (full_chunk) {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
+                    for (int k = 0; k < kSub; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
                 } else {
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                    for (int k = 0; k < kSub; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
                 }
                 sum += acc_s;
+                }
             }
             rowstat[cg * kM + lane_idx] = make_float2(m, sum);
             sm100::named_bar_sync(1, kEpiWarps * 32);
@@ -234,25 +261,32 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
             sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
             sm100::tc_fence_after();
-            sm100::tmem_ld32(lane_addr + acc * kN, l);
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tempty + acc);
-            // per entry: u = l*c1 - mb_r (log2 of exp(logit - max)), below <=> u < t2_r,
-            // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
-            // as a float (set + add).  The same operation order in every branch,
-            // so identical key columns give bit-identical mass.
             // exact mode: an entry whose decision u < t2 is within `band` of flipping
             // (fp32 logits vs the reference's float64 dots) is not counted here but
             // listed for a float64 re-decision.  band = 0: plain decisions.
             const float band = EXACT ? a.band : 0.f;
-            float csum = 0.f, cntf = 0.f, cnth = 0.f;   // cnth - cntf: entries inside the band
-            const float4* mb4 = reinterpret_cast<const float4*>(c_mb + r0);
-            const float4* is4 = reinterpret_cast<const float4*>(c_is + r0);
+            float csum = 0.f;
+            int cnt = 0;
+#pragma unroll
+            for (int h = 0; h < kNSub; ++h) {
+            const int rh = r0 + h * kSub;                        // first row of this sub-chunk
+            float cntf = 0.f, cnth = 0.f;                        // cnth - cntf: entries inside the band
+            tmem_ld(lane_addr + acc * kN + h * kSub, l);
+            if (h == kNSub - 1) {
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + acc);
+            }
+            // per entry: u = l*c1 - mb_r (log2 of exp(logit - max)), below <=> u < t2_r,
+            // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
+            // as a float (set + add).  The same operation order in every branch,
+            // so identical key columns give bit-identical mass.
+            const float4* mb4 = reinterpret_cast<const float4*>(c_mb + rh);
+            const float4* is4 = reinterpret_cast<const float4*>(c_is + rh);
             if (all_visible && r_first + r0 + 31 < R) {   // every row real and every key visible
                 const float t2c = a.t_star * kLog2e, t2lo = t2c - band;
 #pragma unroll
-                for (int q4 = 0; q4 < 8; ++q4) {
+                for (int q4 = 0; q4 < kSub / 4; ++q4) {
                     const float4 mb = mb4[q4], iv = is4[q4];
                     const float mbv[4] = {mb.x, mb.y, mb.z, mb.w}, ivv[4] = {iv.x, iv.y, iv.z, iv.w};
 #pragma unroll
@@ -265,28 +299,27 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const bool vis = all_visible || j <= c_lim[r0 + k];
-                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    const float t2 = c_t2[r0 + k];
+                for (int k = 0; k < kSub; ++k) {
+                    const bool vis = all_visible || j <= c_lim[rh + k];
+                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
+                    const float t2 = c_t2[rh + k];
                     cntf += (vis && u < t2 - band) ? 1.f : 0.f;
                     if (EXACT) cnth += (vis && u < t2 + band) ? 1.f : 0.f;
-                    csum = vis ? fmaf(ex2(u), c_is[r0 + k], csum) : csum;
+                    csum = vis ? fmaf(ex2(u), c_is[rh + k], csum) : csum;
                 }
             }
-            int cnt = (int)cntf;
             if (EXACT && __any_sync(kFull, cnth != cntf)) {
                 // reserve this thread's entries with one atomic, then write them
                 const int nf = (int)(cnth - cntf);
                 int at = nf ? atomicAdd(a.fix_counts + 1, nf) : 0;
 #pragma unroll
-                for (int k = 0; k < 32; ++k) {   // static indices: l stays in registers
-                    const bool vis = j < a.n && (all_visible || j <= c_lim[r0 + k]);
-                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    const float t2 = c_t2[r0 + k];
+                for (int k = 0; k < kSub; ++k) {   // static indices: l stays in registers
+                    const bool vis = j < a.n && (all_visible || j <= c_lim[rh + k]);
+                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
+                    const float t2 = c_t2[rh + k];
                     if (nf && vis && u >= t2 - band && u < t2 + band) {
                         if (at < a.cap) {
-                            a.flag[at] = make_int4(s, (int)(r_first + r0 + k), j, 1);
+                            a.flag[at] = make_int4(s, (int)(r_first + rh + k), j, 1);
                         } else {   // list full: keep the fp32 decision
                             atomicAdd(a.fix_counts + 2, 1);
                             cnt += u < t2 ? 1 : 0;
@@ -295,20 +328,23 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     }
                 }
             }
+            cnt += (int)cntf;
+            if (!one_head) {
+#pragma unroll
+                for (int k = 0; k < kSub; ++k) {
+                    const bool vis = all_visible || j <= c_lim[rh + k];
+                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
+                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[rh + k] - band) ? 1 : 0);
+                    if (lane == 0 && tot) atomicAdd(hcnt + (int)((r_first + rh + k) / a.w - head0), tot);
+                }
+            }
+            }
             if (j < a.n) colp[j] = csum;
             if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
             // per-head totals (warp reduce, one shared atomic per warp)
-            if (one_head) {
+            if (one_head) {   // (mixed-head groups were counted row by row above)
                 const int tot = __reduce_add_sync(kFull, cnt);
                 if (lane == 0 && tot) atomicAdd(hcnt + (int)(rg / a.w - head0), tot);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    const bool vis = all_visible || j <= c_lim[r0 + k];
-                    const float u = fmaf(l[k], c1, -c_mb[r0 + k]);
-                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[r0 + k] - band) ? 1 : 0);
-                    if (lane == 0 && tot) atomicAdd(hcnt + (int)((rg + k) / a.w - head0), tot);
-                }
             }
         }
         // columns no row of this block can see
