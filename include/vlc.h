@@ -154,6 +154,15 @@ VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, 
                     int32_t kv_heads, int32_t group, int32_t head_dim, double scale, int32_t chained,
                     float *out, void *stream);
 
+/*
+ * Staging helper: `height` rows of `width` bytes, `spitch` / `dpitch` bytes
+ * apart, host or device to host or device, ordered on `stream` (asynchronous
+ * from pinned host memory).  Used to stream a strided slab of the host inputs
+ * (e.g. the rows of a group of decode steps) while earlier stages compute.
+ */
+VLC_API int vlc_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
+                    int64_t height, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

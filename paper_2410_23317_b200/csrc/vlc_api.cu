@@ -218,6 +218,15 @@ int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head
     return cuda_status(vlc::launch_gather(a, (cudaStream_t)stream), "gather");
 }
 
+int vlc_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
+                void* stream) {
+    if (!dst || !src) return fail(VLC_EINVAL, "copy_2d: null pointer");
+    if (width < 0 || height < 0 || dpitch < width || spitch < width) return fail(VLC_EINVAL, "copy_2d: bad extent");
+    if (width == 0 || height == 0) return VLC_OK;
+    return cuda_status(cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width, (size_t)height,
+                                         cudaMemcpyDefault, (cudaStream_t)stream), "copy_2d");
+}
+
 int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const void* v_new,
                     int64_t kv_stride, void* k_cache, void* v_cache, int64_t cache_rows,
                     const int64_t* cache_off,

@@ -262,31 +262,35 @@ class VLCache:
                   _ptr(self.out), _stream())
         return self.out
 
-    def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None, row0=None):
-        """n_steps decode steps; with graph=True the launch sequence is captured
-        once into a CUDA graph (per input pointers) and replayed."""
+    def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None, row0=None, first_step=0):
+        """Decode steps first_step .. first_step + n_steps - 1 (default: all of
+        them); with graph=True the launch sequence is captured once into a CUDA
+        graph (per input pointers and step range) and replayed."""
         import torch
 
-        n = self.decode_steps if n_steps is None else int(n_steps)
+        t0 = int(first_step)
+        n = self.decode_steps - t0 if n_steps is None else int(n_steps)
+        if not (0 <= t0 and n >= 1 and t0 + n <= self.decode_steps):
+            raise ValidationError(f"steps: [{t0}, {t0 + n}) outside [0, {self.decode_steps})")
         if outputs is not None or not graph:
-            for t in range(n):
+            for t in range(t0, t0 + n):
                 self.decode_step(q_dec, keys, values, t, row0=row0)
                 if outputs is not None:
                     outputs.append(self.out.clone())
             return self.out
-        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), n, row0)
+        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), t0, n, row0)
         g = self._graphs.get(key)
         if g is None:
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
-                for t in range(n):   # warm-up launch outside capture
-                    self.decode_step(q_dec, keys, values, t, chained=t > 0, row0=row0)
+                for t in range(t0, t0 + n):   # warm-up launch outside capture
+                    self.decode_step(q_dec, keys, values, t, chained=t > t0, row0=row0)
             torch.cuda.current_stream().wait_stream(side)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                for t in range(n):
-                    self.decode_step(q_dec, keys, values, t, chained=t > 0, row0=row0)
+                for t in range(t0, t0 + n):
+                    self.decode_step(q_dec, keys, values, t, chained=t > t0, row0=row0)
             self._graphs[key] = g
         g.replay()
         return self.out
@@ -352,18 +356,32 @@ class VLCache:
                     ev = torch.cuda.Event()
                     ev.record(cs)
                     groups.append((b, l0, l1, ev))
-            for dst, src in ((d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
-                dst.copy_(src, non_blocking=True)
-            ev_dec = torch.cuda.Event()
-            ev_dec.record(cs)
+            # decode inputs in step groups, so the first decode steps run while
+            # the later groups' rows are still crossing PCIe
+            n = q_dec.shape[3]
+            per_s = -(-n // max(1, int(chunks)))
+            steps = []
+            for s0 in range(0, n, per_s):
+                s1 = min(n, s0 + per_s)
+                for dst, src in ((d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
+                    rows = src.numel() // (n * s.d)           # B*L*H
+                    pitch = n * s.d * 2
+                    _lib.call("vlc_copy_2d", dst.data_ptr() + s0 * s.d * 2, pitch, src.data_ptr() + s0 * s.d * 2,
+                              pitch, (s1 - s0) * s.d * 2, rows, cs.cuda_stream)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                steps.append((s0, s1, ev))
         for b, l0, l1, ev in groups:
             comp.wait_event(ev)
             self.score_stats_layers(d_qw, d_k, b, l0, l1)
         self.allocate()
         self.select()
         self.gather(d_k, v_prompt)             # keys from the device copy, values zero-copy
-        comp.wait_event(ev_dec)
-        self.decode(d_qd, d_kn, d_vn, row0=0)
+        for s0, s1, ev in steps:
+            if s0 >= self.decode_steps:
+                break
+            comp.wait_event(ev)
+            self.decode(d_qd, d_kn, d_vn, row0=0, first_step=s0, n_steps=min(s1, self.decode_steps) - s0)
         h_counts.copy_(self.kept_counts, non_blocking=True)
         h_out.copy_(self.out, non_blocking=True)
         copied = sum(t.numel() * 2 for t in (q_win, k_prompt, q_dec, k_dec, v_dec))

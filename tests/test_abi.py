@@ -15,7 +15,7 @@ from paper_2410_23317_b200.errors import ValidationError
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "vlc.h")).read()
-    return sorted(set(re.findall(r"\b(vlc_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(vlc_[a-z_0-9]+)\s*\(", text)))
 
 
 def test_library_loads_and_exports_every_header_symbol():
