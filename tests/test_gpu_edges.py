@@ -165,8 +165,9 @@ def test_head_sharded_budgets_equal_unsharded():
 @pytest.mark.parametrize("alpha", [0.01, 0.2, 1.0])
 def test_sweep_16k_context_properties(alpha):
     """SWEEP shapes (16,384-token prompt) on 2 layers: budgets against the
-    oracle allocation of the device's own gamma', sorted kept sets with the
-    recent reserve, and decode against the oracle on one layer."""
+    oracle allocation of the device's own gamma' and against the oracle's own
+    stats pass (counts, k_l, kept indices), sorted kept sets with the recent
+    reserve, and decode against the oracle on one layer."""
     import math
 
     L, HQ, HKV, D, M, TAU = 2, 32, 8, 128, 16384, 64
@@ -179,6 +180,15 @@ def test_sweep_16k_context_properties(alpha):
     _, _, kc = O.allocate_sparsity_aware(gm, alpha, M)
     counts = eng.kept_counts.cpu().numpy()
     np.testing.assert_array_equal(counts, kc)
+    # and against the oracle's own stats pass: counts, budgets and kept indices
+    import os
+
+    ref = O.compression_pass(host[0]["q_win"], host[0]["keys"], M, HQ // HKV, alpha=alpha,
+                             threads=len(os.sched_getaffinity(0)))
+    ref_below = np.array([[ref["stats"][(l, h)][3].sum() for h in range(HQ)] for l in range(L)])
+    np.testing.assert_array_equal(eng.below_head.view(L, HQ).cpu().numpy(), ref_below)
+    np.testing.assert_array_equal(counts, ref["kept_counts"])
+    check_kept_sets(eng.kept_sets()[0], ref["kept"], ref["scores"], ref["kept_counts"])
     sc = eng.scores.view(L, HKV, M).cpu().numpy()
     kept = eng.kept_sets()[0]
     for l in range(L):
