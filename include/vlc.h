@@ -51,7 +51,7 @@ VLC_API const char *vlc_last_error(void);
 VLC_API float vlc_threshold_logit(double p);
 
 /* Rows of col_partial per slot for a window of `rows` = G*w rows (one
- * partial per 32 window rows; 4 per 128-row block). */
+ * partial per 64 window rows; 2 per 128-row block). */
 VLC_API int64_t vlc_score_partials(int64_t rows);
 
 /*
@@ -60,7 +60,7 @@ VLC_API int64_t vlc_score_partials(int64_t rows);
  * (absolute index q_base + i) against keys [0, min(n_keys, q_base+i+1)).
  *   row_max, row_sum : f32 [slots*G*w]       (_core.pyx:142-155)
  *   col_partial      : f32 [slots, vlc_score_partials(G*w), n_keys] column
- *                      mass of each 32-row group (their sum is the slot's
+ *                      mass of each 64-row half (their sum is the slot's
  *                      col_score summed over its G heads)
  *   below_head       : u64 [slots*G]  entries with exp(l - max) < p, per head
  *   below_col        : i32 [slots, n_keys] or NULL (per-column counts)

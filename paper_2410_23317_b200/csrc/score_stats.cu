@@ -17,8 +17,8 @@
 
 namespace vlc {
 
-// col_partial rows per slot: 4 row groups of 32 rows per 128-row block
-int score_partials(int64_t rows) { return (int)(4 * ((rows + 127) / 128)); }
+// col_partial rows per slot: 2 row halves of 64 rows per 128-row block
+int score_partials(int64_t rows) { return (int)(2 * ((rows + 127) / 128)); }
 
 namespace {
 

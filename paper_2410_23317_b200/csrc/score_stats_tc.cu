@@ -3,15 +3,17 @@
 // reference: pkg/src/vlcache/_kernels/_core.pyx:110-242 (two-pass tiled
 // statistics) for all G query heads of a KV head at once.
 //
-// CTA = (slot, block of 128 window rows).  Warp roles (384 threads):
+// CTA = (slot, block of 128 window rows).  Warp roles (640 threads):
 //   warp 0      TMA producer: the Q block once, then every 128-key tile of the
 //               slot twice (pass 1, pass 2) into a 3-stage swizzled ring
 //   warp 1      MMA issuer, M=128 x N=128, K = head_dim, bf16 in, fp32
-//               accumulate in TMEM (two accumulator stages, 256 columns).
+//               accumulate in TMEM (four accumulator stages, all 512 columns).
 //               Pass 1 computes Q K^T (rows on TMEM lanes), pass 2 K Q^T
 //               (keys on TMEM lanes) from the same shared-memory operands.
 //   warp 2      TMEM allocator
-//   warps 4-11  epilogue, tcgen05.ld 32 columns at a time:
+//   warps 4-19  epilogue in two sets of 8, set p reading the tiles it = p
+//               (mod 2) from accumulator stages p, p + 2; tcgen05.ld 32
+//               columns at a time; 112 registers each (setmaxnreg):
 //               pass 1: thread = window row -> running max / sum (serial);
 //               pass 2: thread = key -> column mass and below-threshold
 //               counts, serial over the block's rows, so neither pass needs a
@@ -39,10 +41,15 @@ constexpr int kN = 128;          // keys per tile (UMMA N)
 #endif
 constexpr int kStages = VLC_K1_STAGES;   // K tile ring
 constexpr int kSub = VLC_K1_SUB;         // TMEM columns an epilogue thread holds at a time (16 / 32)
-constexpr int kNSub = 32 / kSub;
-constexpr int kEpiWarps = 16;    // 4 per TMEM lane quarter, one 32-column group each
+constexpr int kEpiWarps = 16;    // two sets of 8, one per accumulator stage
+constexpr int kSetWarps = kEpiWarps / 2;   // 4 lane quarters x 2 column halves of 64
+constexpr int kCh = 64 / kSub;             // TMEM loads per warp and tile
 constexpr int kThreads = 128 + kEpiWarps * 32;
-constexpr uint32_t kTmemCols = 2 * kN;
+#ifndef VLC_K1_ACC
+#define VLC_K1_ACC 4
+#endif
+constexpr int kAcc = VLC_K1_ACC;           // accumulator stages (2 or 4; set p owns stages = p mod 2)
+constexpr uint32_t kTmemCols = kAcc * kN;
 
 template <int D>
 struct Layout {
@@ -80,9 +87,9 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // small state in static shared memory (plain LDS/STS, not generic accesses)
-    __shared__ uint64_t full[kStages], empty[kStages], qfull[1], tfull[2], tempty[2];
+    __shared__ uint64_t full[kStages], empty[kStages], qfull[1], tfull[kAcc], tempty[kAcc];
     __shared__ uint32_t tmem_slot[1];
-    __shared__ float2 rowstat[4 * kM];                  // (max, sum) per column group and row
+    __shared__ float2 rowstat[4 * kM];                  // (max, sum) per (set, column half) and row
     __shared__ __align__(16) float c_mb[kM];            // row max (raw dot) * c1
     __shared__ __align__(16) float c_is[kM];            // 1 / row sum (0: no row)
     __shared__ __align__(16) float c_t2[kM];            // threshold on u (-inf: no row)
@@ -103,7 +110,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int i = 0; i < kStages; ++i) { sm100::mbar_init(full + i, 1); sm100::mbar_init(empty + i, 1); }
         sm100::mbar_init(qfull, 1);
-        for (int i = 0; i < 2; ++i) { sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kEpiWarps); }
+        for (int i = 0; i < kAcc; ++i) { sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kSetWarps); }
         sm100::fence_barrier_init();
         sm100::fence_proxy_async();
     }
@@ -114,60 +121,69 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     sm100::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0 && lane == 0) {
-        // ------------------------------------------------ TMA producer
-        sm100::tma_prefetch(&qmap);
-        sm100::tma_prefetch(&kmap);
-        sm100::mbar_expect_tx(qfull, LY::kQBytes);
-        for (int kb = 0; kb < LY::KB; ++kb)
-            sm100::tma_load_2d(smem + kb * LY::kQRegion, &qmap, qfull, kb * 64, (int)(s * R + r_first));
-        for (int it = 0; it < iters; ++it) {
-            const int st = it % kStages;
-            const uint32_t ph = (it / kStages) & 1;
-            const int t = it < T ? it : it - T;
-            sm100::mbar_wait(empty + st, ph ^ 1);
-            sm100::mbar_expect_tx(full + st, LY::kKBytes);
-            uint8_t* kdst = smem + LY::kQBytes + st * LY::kKBytes;
+    // registers: the control warpgroup (warps 0-3) gives its share to the four
+    // epilogue warpgroups (launch 96 x 640 = 32 x 128 + 112 x 512)
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n");
+        if (warp == 0 && lane == 0) {
+            // ------------------------------------------------ TMA producer
+            sm100::tma_prefetch(&qmap);
+            sm100::tma_prefetch(&kmap);
+            sm100::mbar_expect_tx(qfull, LY::kQBytes);
             for (int kb = 0; kb < LY::KB; ++kb)
-                sm100::tma_load_2d(kdst + kb * LY::kKRegion, &kmap, full + st, kb * 64,
-                                   (int)(s * a.T + (int64_t)t * kN));
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ------------------------------------------------ MMA issuer
-        // pass 1: D[row, key] = Q K^T (rows on TMEM lanes); pass 2: D[key, row]
-        // = K Q^T (keys on TMEM lanes) -- same operands, swapped roles
-        constexpr uint32_t idesc = sm100::idesc_bf16_f32(kM, kN);
-        const uint32_t q_addr = sm100::smem_u32(smem);
-        sm100::mbar_wait(qfull, 0);
-        for (int it = 0; it < iters; ++it) {
-            const int st = it % kStages;
-            const uint32_t ph = (it / kStages) & 1;
-            const int acc = it & 1;
-            const uint32_t aph = (it >> 1) & 1;
-            sm100::mbar_wait(tempty + acc, aph ^ 1);
-            sm100::mbar_wait(full + st, ph);
-            sm100::tc_fence_after();
-            const uint32_t k_addr = sm100::smem_u32(smem + LY::kQBytes + st * LY::kKBytes);
-            const bool rows_on_lanes = it < T;
-#pragma unroll
-            for (int kb = 0; kb < LY::KB; ++kb) {
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {   // 4 x 16 elements = one 128 B swizzle row
-                    const uint64_t qd = sm100::sdesc_k_sw128(q_addr + kb * LY::kQRegion + kk * 32);
-                    const uint64_t kd = sm100::sdesc_k_sw128(k_addr + kb * LY::kKRegion + kk * 32);
-                    sm100::mma_bf16(tmem + acc * kN, rows_on_lanes ? qd : kd, rows_on_lanes ? kd : qd, idesc,
-                                    (kb | kk) != 0);
-                }
+                sm100::tma_load_2d(smem + kb * LY::kQRegion, &qmap, qfull, kb * 64, (int)(s * R + r_first));
+            for (int it = 0; it < iters; ++it) {
+                const int st = it % kStages;
+                const uint32_t ph = (it / kStages) & 1;
+                const int t = it < T ? it : it - T;
+                sm100::mbar_wait(empty + st, ph ^ 1);
+                sm100::mbar_expect_tx(full + st, LY::kKBytes);
+                uint8_t* kdst = smem + LY::kQBytes + st * LY::kKBytes;
+                for (int kb = 0; kb < LY::KB; ++kb)
+                    sm100::tma_load_2d(kdst + kb * LY::kKRegion, &kmap, full + st, kb * 64,
+                                       (int)(s * a.T + (int64_t)t * kN));
             }
-            sm100::mma_commit(empty + st);   // K stage reusable once these MMAs retire
-            sm100::mma_commit(tfull + acc);  // accumulator ready for the epilogue
+        } else if (warp == 1 && lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            // pass 1: D[row, key] = Q K^T (rows on TMEM lanes); pass 2: D[key, row]
+            // = K Q^T (keys on TMEM lanes) -- same operands, swapped roles
+            constexpr uint32_t idesc = sm100::idesc_bf16_f32(kM, kN);
+            const uint32_t q_addr = sm100::smem_u32(smem);
+            sm100::mbar_wait(qfull, 0);
+            for (int it = 0; it < iters; ++it) {
+                const int st = it % kStages;
+                const uint32_t ph = (it / kStages) & 1;
+                const int acc = it % kAcc;
+                const uint32_t aph = (it / kAcc) & 1;
+                sm100::mbar_wait(tempty + acc, aph ^ 1);
+                sm100::mbar_wait(full + st, ph);
+                sm100::tc_fence_after();
+                const uint32_t k_addr = sm100::smem_u32(smem + LY::kQBytes + st * LY::kKBytes);
+                const bool rows_on_lanes = it < T;
+#pragma unroll
+                for (int kb = 0; kb < LY::KB; ++kb) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {   // 4 x 16 elements = one 128 B swizzle row
+                        const uint64_t qd = sm100::sdesc_k_sw128(q_addr + kb * LY::kQRegion + kk * 32);
+                        const uint64_t kd = sm100::sdesc_k_sw128(k_addr + kb * LY::kKRegion + kk * 32);
+                        sm100::mma_bf16(tmem + acc * kN, rows_on_lanes ? qd : kd, rows_on_lanes ? kd : qd, idesc,
+                                        (kb | kk) != 0);
+                    }
+                }
+                sm100::mma_commit(empty + st);   // K stage reusable once these MMAs retire
+                sm100::mma_commit(tfull + acc);  // accumulator ready for the epilogue
+            }
         }
-    } else if (warp >= 4) {
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
         // ------------------------------------------------ epilogue
-        // warp -> (TMEM lane quarter `sub`, 32-column group `cg`)
-        const int ew = warp - 4, sub = warp & 3, cg = ew >> 2;
+        // Two warp sets, set p taking tiles it = p (mod 2) from accumulator stages
+        // p and p + 2, so one set's TMEM-load latency overlaps the other's math and
+        // the MMA runs a tile ahead of each set.  Within a set,
+        // warp -> (TMEM lane quarter `sub`, 64-column half `half`).
+        const int ew = warp - 4, sub = warp & 3, set = ew >> 3, half = (ew >> 2) & 1;
         const int lane_idx = 32 * sub + lane;                  // TMEM lane of this thread
-        const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + cg * 32;
+        const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + half * 64;
         const float c1 = a.inv_scale * kLog2e;
         float l[kSub];
 
@@ -178,19 +194,19 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int64_t i = row_ok ? r % a.w : 0;
             const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
             float m = -INFINITY, sum = 0.f;
-            for (int it = 0; it < T; ++it) {
-                const int acc = it & 1;
-                sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
+            for (int it = set; it < T; it += 2) {
+                const int acc = it % kAcc;
+                sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
                 sm100::tc_fence_after();
 #pragma unroll
-                for (int h = 0; h < kNSub; ++h) {
+                for (int h = 0; h < kCh; ++h) {
                 tmem_ld(lane_addr + acc * kN + h * kSub, l);
-                if (h == kNSub - 1) {
+                if (h == kCh - 1) {
                     sm100::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the chunk now
+                    if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the tile now
                 }
-                const int valid = (int)imax(0, imin(kSub, row_end - ((int64_t)it * kN + cg * 32 + h * kSub)));
+                const int valid = (int)imax(0, imin(kSub, row_end - ((int64_t)it * kN + half * 64 + h * kSub)));
                 const bool full_chunk = __all_sync(kFull, valid == kSub);
                 float cmax;
                 if (full_chunk) {
@@ -205,20 +221,20 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     m = cmax;
                 }
                 const float mb = m * c1;
-                float acc_s = 0.f;
+                float acc_s[4] = {0.f, 0.f, 0.f, 0.f};   // four chains: ILP for the adds
                 if (full_chunk) {
 #pragma unroll
-                    for (int k = 0; k < kSub; ++k) acc_s += ex2(fmaf(l[k], c1, -mb));
+                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += ex2(fmaf(l[k], c1, -mb));
                 } else {
 #pragma unroll
-                    for (int k = 0; k < kSub; ++k) acc_s += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
                 }
-                sum += acc_s;
+                sum += (acc_s[0] + acc_s[1]) + (acc_s[2] + acc_s[3]);
                 }
             }
-            rowstat[cg * kM + lane_idx] = make_float2(m, sum);
+            rowstat[(set * 2 + half) * kM + lane_idx] = make_float2(m, sum);
             sm100::named_bar_sync(1, kEpiWarps * 32);
-            if (cg == 0) {
+            if (ew < 4) {
                 float M = -INFINITY;
 #pragma unroll
                 for (int g4 = 0; g4 < 4; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
@@ -246,44 +262,44 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         }
 
         // ---- pass 2 (thread = key): column mass and below-threshold counts over
-        //   the 32 rows of group cg.  u = l*c1 - mb_r ~ log2(exp(logit - max));
+        //   the 64 rows of this half.  u = l*c1 - mb_r ~ log2(exp(logit - max));
         //   below <=> u < t* log2e; mass = 2^(u - log2 S_r).  Serial per key: no
         //   cross-lane reduction, and every key column follows the same order.
-        //   Each row group writes its own partial row of col_partial (no barrier).
-        const int r0 = cg * 32;
+        //   Each half writes its own partial row of col_partial (no barrier).
+        const int r0 = half * 64;
         const int64_t rg = r_first + r0;
-        const bool one_head = rg / a.w == (rg + 31) / a.w;
-        float* colp = a.col_partial + ((int64_t)s * nparts + rb * 4 + cg) * a.n;
-        for (int it = T; it < iters; ++it) {
-            const int acc = it & 1;
+        const bool one_head = rg / a.w == (rg + 63) / a.w;
+        float* colp = a.col_partial + ((int64_t)s * nparts + rb * 2 + half) * a.n;
+        for (int it = T + ((T ^ set) & 1); it < iters; it += 2) {
             const int t = it - T;
             const int j = t * kN + lane_idx;                     // this thread's key
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
-            sm100::mbar_wait(tfull + acc, (it >> 1) & 1);
+            const int acc = it % kAcc;
+            sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
             sm100::tc_fence_after();
             // exact mode: an entry whose decision u < t2 is within `band` of flipping
             // (fp32 logits vs the reference's float64 dots) is not counted here but
             // listed for a float64 re-decision.  band = 0: plain decisions.
             const float band = EXACT ? a.band : 0.f;
-            float csum = 0.f;
+            float cs[4] = {0.f, 0.f, 0.f, 0.f};   // mass in four chains (ILP), merged per tile
             int cnt = 0;
 #pragma unroll
-            for (int h = 0; h < kNSub; ++h) {
-            const int rh = r0 + h * kSub;                        // first row of this sub-chunk
-            float cntf = 0.f, cnth = 0.f;                        // cnth - cntf: entries inside the band
+            for (int h = 0; h < kCh; ++h) {
+            const int rh = r0 + h * kSub;                        // first row of this chunk
+            float cf[2] = {0.f, 0.f}, ch[2] = {0.f, 0.f};       // ch - cf: entries inside the band
             tmem_ld(lane_addr + acc * kN + h * kSub, l);
-            if (h == kNSub - 1) {
+            if (h == kCh - 1) {
                 sm100::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(tempty + acc);
             }
             // per entry: u = l*c1 - mb_r (log2 of exp(logit - max)), below <=> u < t2_r,
             // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
-            // as a float (set + add).  The same operation order in every branch,
-            // so identical key columns give bit-identical mass.
+            // as a float (set + add).  The same operation order in every branch
+            // (chain k & 3 for row k), so identical key columns give bit-identical mass.
             const float4* mb4 = reinterpret_cast<const float4*>(c_mb + rh);
             const float4* is4 = reinterpret_cast<const float4*>(c_is + rh);
-            if (all_visible && r_first + r0 + 31 < R) {   // every row real and every key visible
+            if (all_visible && r_first + rh + kSub - 1 < R) {   // every row real and every key visible
                 const float t2c = a.t_star * kLog2e, t2lo = t2c - band;
 #pragma unroll
                 for (int q4 = 0; q4 < kSub / 4; ++q4) {
@@ -292,9 +308,9 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
-                        cntf += u < t2lo ? 1.f : 0.f;
-                        if (EXACT) cnth += u < t2c + band ? 1.f : 0.f;
-                        csum = fmaf(ex2(u), ivv[e], csum);
+                        cf[e & 1] += u < t2lo ? 1.f : 0.f;
+                        if (EXACT) ch[e & 1] += u < t2c + band ? 1.f : 0.f;
+                        cs[e] = fmaf(ex2(u), ivv[e], cs[e]);
                     }
                 }
             } else {
@@ -303,11 +319,12 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     const bool vis = all_visible || j <= c_lim[rh + k];
                     const float u = fmaf(l[k], c1, -c_mb[rh + k]);
                     const float t2 = c_t2[rh + k];
-                    cntf += (vis && u < t2 - band) ? 1.f : 0.f;
-                    if (EXACT) cnth += (vis && u < t2 + band) ? 1.f : 0.f;
-                    csum = vis ? fmaf(ex2(u), c_is[rh + k], csum) : csum;
+                    cf[k & 1] += (vis && u < t2 - band) ? 1.f : 0.f;
+                    if (EXACT) ch[k & 1] += (vis && u < t2 + band) ? 1.f : 0.f;
+                    cs[k & 3] = vis ? fmaf(ex2(u), c_is[rh + k], cs[k & 3]) : cs[k & 3];
                 }
             }
+            const float cntf = cf[0] + cf[1], cnth = ch[0] + ch[1];
             if (EXACT && __any_sync(kFull, cnth != cntf)) {
                 // reserve this thread's entries with one atomic, then write them
                 const int nf = (int)(cnth - cntf);
@@ -339,16 +356,17 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 }
             }
             }
-            if (j < a.n) colp[j] = csum;
+            if (j < a.n) colp[j] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
             if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
             // per-head totals (warp reduce, one shared atomic per warp)
-            if (one_head) {   // (mixed-head groups were counted row by row above)
+            if (one_head) {   // (mixed-head halves were counted row by row above)
                 const int tot = __reduce_add_sync(kFull, cnt);
                 if (lane == 0 && tot) atomicAdd(hcnt + (int)(rg / a.w - head0), tot);
             }
         }
         // columns no row of this block can see
-        for (int64_t jj = (int64_t)T * kN + lane_idx; jj < a.n; jj += kN) colp[jj] = 0.f;
+        if (set == 0)
+            for (int64_t jj = (int64_t)T * kN + lane_idx; jj < a.n; jj += kN) colp[jj] = 0.f;
         sm100::named_bar_sync(1, kEpiWarps * 32);
         const int nheads = (int)(r_last / a.w - head0 + 1);
         for (int h = ew * 32 + lane; h < nheads; h += kEpiWarps * 32)
@@ -372,7 +390,7 @@ cudaError_t launch_tc_e(const ScoreArgs& a, int nparts, cudaStream_t st) {
     const size_t sm = Layout<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid(nparts / 4, a.slots);
+    dim3 grid(nparts / 2, a.slots);
     score_stats_tc<D, EXACT><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nparts);
     return cudaGetLastError();
 }

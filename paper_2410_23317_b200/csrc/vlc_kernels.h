@@ -35,7 +35,7 @@ struct ScoreArgs {
     float inv_scale, t_star;
     float* row_max;                    // [slots*R]
     float* row_sum;                    // [slots*R]
-    float* col_partial;                // [slots, score_partials(G*w), n] column sums per 32-row group
+    float* col_partial;                // [slots, score_partials(G*w), n] column sums per 64-row half
     unsigned long long* below_head;    // [slots*G]  (zeroed by the launcher)
     int* below_col;                    // optional [slots, n] (zeroed by the launcher)
     // exact mode (fix != nullptr): entries whose below-threshold decision is

@@ -76,7 +76,7 @@ class Shape:
     @property
     def nrb(self) -> int:
         """col_partial rows per slot (vlc_score_partials)."""
-        return 4 * ((self.G * self.w + _ROW_BLOCK - 1) // _ROW_BLOCK)
+        return 2 * ((self.G * self.w + _ROW_BLOCK - 1) // _ROW_BLOCK)
 
     @property
     def causal_per_head(self) -> int:

@@ -11,7 +11,7 @@ ncu --graph-profiling node --metrics gpu__time_duration.sum --clock-control none
 ncu --graph-profiling node --set full --import-source on --clock-control none -k regex:decode_kernel -s 150 -c 1 \
     -o $O/k5_$TAG python tools/k5_graph_run.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:score_stats_tc -s 1 -c 1 \
-    -o $O/k1_$TAG python tools/profile_step.py > /dev/null 2>&1
+    -o $O/k1_$TAG env GEN=1 python tools/profile_step.py > /dev/null 2>&1
 ncu --graph-profiling node --cache-control none --clock-control none -k regex:decode_kernel -s 150 -c 5 \
     --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
     python tools/k5_graph_run.py > $O/k5_traffic_$TAG.csv 2>&1
