@@ -163,6 +163,28 @@ VLC_API int vlc_decode_step(const void *q, int64_t q_stride, const void *k_new, 
 VLC_API int vlc_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spitch, int64_t width,
                     int64_t height, void *stream);
 
+/*
+ * Analysis rows.  Dense causal softmax of fp32
+ * query rows against fp32 keys: row r (absolute query first_row + r) of head h
+ * sees keys [0, min(key_limit, first_row + r + 1)) of KV head h / group;
+ *   probs[h, r, j] = double(e_j) / sum double(e),  e_j = float32 exp(l_j - max l),
+ *   l_j = float32(float64 dot(q, k_j) * (1/sqrt(d)))
+ * exactly as reference attention.py:72-90 (dense_attention_rows, key_limit =
+ * first_row + rows) and evaluate.py:78-104 (oracle_scores, key_limit = m).
+ * q: f32 [heads, rows, d]; k: f32 [heads/group, key_rows, d] (16-byte aligned
+ * when d % 4 == 0, the vector path).
+ * probs: f64 [heads*rows, out_cols] or NULL (zeros past the visible keys).
+ * mass: f64 [heads*rows, 3] or NULL: after the threshold filter (keep
+ * prob >= filter_p * row max; sparsity.py:46-66) the mass on prompt columns
+ * [vision_start, vision_end), on the other prompt columns [0, prompt_len), and
+ * their sum (evaluate.py:161-185).  Visible key span <= ~55K (shared memory).
+ */
+VLC_API int vlc_attention_rows(const float *q, const float *k, int32_t heads, int32_t group,
+                    int32_t head_dim, int64_t rows, int64_t key_rows, int64_t first_row,
+                    int64_t key_limit, int64_t out_cols, double *probs, double filter_p,
+                    int64_t prompt_len, int64_t vision_start, int64_t vision_end, double *mass,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -218,6 +218,33 @@ int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head
     return cuda_status(vlc::launch_gather(a, (cudaStream_t)stream), "gather");
 }
 
+int vlc_attention_rows(const float* q, const float* k, int32_t heads, int32_t group, int32_t head_dim,
+                       int64_t rows, int64_t key_rows, int64_t first_row, int64_t key_limit, int64_t out_cols,
+                       double* probs, double filter_p, int64_t prompt_len, int64_t vision_start,
+                       int64_t vision_end, double* mass, void* stream) {
+    if (!q || !k) return fail(VLC_EINVAL, "attention_rows: null pointer");
+    if (!probs && !mass) return fail(VLC_EINVAL, "attention_rows: nothing to write (probs and mass NULL)");
+    if (heads < 1 || group < 1 || heads % group || rows < 1 || first_row < 0 || key_limit < 1 || out_cols < 0)
+        return fail(VLC_EINVAL, "attention_rows: bad shape");
+    if (head_dim < 1 || head_dim > 4096) return fail(VLC_EINVAL, "head_dim: must be in [1, 4096], got %d", head_dim);
+    const int64_t span = std::min(key_limit, first_row + rows);
+    if (span > key_rows) return fail(VLC_EINVAL, "attention_rows: rows see %lld keys, key_rows is %lld",
+                                     (long long)span, (long long)key_rows);
+    if (vlc::attention_rows_smem(head_dim, span) > 227 * 1024)
+        return fail(VLC_EUNSUPPORTED, "attention_rows: %lld visible keys exceed shared memory", (long long)span);
+    if (mass && (vision_start < 0 || vision_end < vision_start || prompt_len < 0))
+        return fail(VLC_EINVAL, "attention_rows: bad modality range");
+    if (head_dim % 4 == 0 && ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k)) & 15))
+        return fail(VLC_EINVAL, "attention_rows: q / k must be 16-byte aligned when head_dim %% 4 == 0");
+    vlc::RowsArgs a{};
+    a.q = q; a.k = k; a.heads = heads; a.group = group; a.d = head_dim; a.rows = rows; a.key_rows = key_rows;
+    a.first_row = first_row; a.key_limit = key_limit; a.out_cols = out_cols;
+    a.inv_scale = 1.0 / std::sqrt((double)head_dim);
+    a.probs = probs; a.filter_p = filter_p; a.prompt_len = prompt_len;
+    a.vis_start = vision_start; a.vis_end = vision_end; a.mass = mass;
+    return cuda_status(vlc::launch_attention_rows(a, (cudaStream_t)stream), "attention_rows");
+}
+
 int vlc_copy_2d(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width, int64_t height,
                 void* stream) {
     if (!dst || !src) return fail(VLC_EINVAL, "copy_2d: null pointer");

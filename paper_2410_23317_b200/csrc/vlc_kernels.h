@@ -127,4 +127,20 @@ struct DecodeArgs {
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 
+// f4 analysis: dense causal softmax rows over fp32 trace rows (eval_rows.cu).
+struct RowsArgs {
+    const float* q;            // f32 [heads, rows, d]: query rows first_row .. first_row+rows-1
+    const float* k;            // f32 [heads / group, key_rows, d]
+    int64_t heads, group, d, rows, key_rows, first_row;
+    int64_t key_limit;         // row r sees keys [0, min(key_limit, first_row + r + 1))
+    int64_t out_cols;          // probs columns written per row (zeros past the visible keys)
+    double inv_scale;          // 1 / sqrt(d) in double
+    double* probs;             // f64 [heads*rows, out_cols] or null
+    double filter_p;           // threshold filter (keep prob >= p * row max) for mass
+    int64_t prompt_len, vis_start, vis_end;
+    double* mass;              // f64 [heads*rows, 3]: filtered (vision, language, prompt) mass, or null
+};
+int64_t attention_rows_smem(int64_t d, int64_t span);
+cudaError_t launch_attention_rows(const RowsArgs& a, cudaStream_t st);
+
 }  // namespace vlc
