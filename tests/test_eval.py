@@ -223,3 +223,24 @@ def test_gpu_eval_edges():
     assert V.contribution(t, 0, 0, win, "vision") == 0.0
     with pytest.raises(V.ValidationError, match="alpha_eval"):
         V.coverage(trace("small"), 0, 0, V.EvalWindow.for_header(trace("small").header, alpha_eval=0.001), "vision")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tau,group", [(64, 4), (128, 2), (192, 1)])
+def test_gpu_batched_head_scores_bit_identical(tau, group):
+    """build_report's one-launch policy scores equal per-head head_scores bit for bit."""
+    import paper_2410_23317_b200 as V
+    from paper_2410_23317_b200.evaluate import _all_head_scores
+
+    spec = dict(num_layers=2, num_query_heads=8, num_kv_heads=8 // group, head_dim=64, prompt_len=700,
+                post_vision_len=tau, decode_len=2, seed=5)
+    tr, _ = generate_trace(GenSpec(**spec))
+    tr = AttentionTrace(header=tr.header, layout=tr.layout, queries=[round_to_bf16(x) for x in tr.queries],
+                        keys=[round_to_bf16(x) for x in tr.keys])
+    got = _all_head_scores(tr, V.PostVision(), V.ScoringConfig())
+    for l in range(2):
+        for q in range(8):
+            np.testing.assert_array_equal(got[l, q], V.head_scores(tr, l, q, V.PostVision()))
+    rep = V.build_report(tr, {"pv": V.PostVision()}, k=50).to_dict()
+    for row in rep["hit_rates"]:
+        assert row["hit_rate"] == V.cache_hit_rate(tr, row["layer"], row["head"], V.PostVision(), 50)
