@@ -32,15 +32,20 @@ VLC_DEV unsigned fkey(float x) {
 }
 VLC_DEV float funkey(unsigned k) { return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k); }
 
-// float32(float64 dot(q_row, k_row) * inv) over bf16 operands
+// float32(float64 dot(q_row, k_row) * inv) over bf16 operands; D known at
+// compile time so all 2*D/8 16-byte loads are in flight before the fp64 chain
+template <int D>
 VLC_DEV float exact_logit(const ScoreArgs& a, int slot, int row, int key) {
     const int64_t R = (int64_t)a.G * a.w;
-    const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)slot * R + row) * a.d);
-    const uint4* k = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) + ((int64_t)slot * a.T + key) * a.d);
+    const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)slot * R + row) * D);
+    const uint4* k = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) + ((int64_t)slot * a.T + key) * D);
+    uint4 qv[D / 8], kv[D / 8];
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) { qv[c] = q[c]; kv[c] = k[c]; }
     double acc = 0.0;
-    for (int c = 0; c < a.d / 8; ++c) {
-        const uint4 qv = q[c], kv = k[c];
-        const uint32_t qa[4] = {qv.x, qv.y, qv.z, qv.w}, ka[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+        const uint32_t qa[4] = {qv[c].x, qv[c].y, qv[c].z, qv[c].w}, ka[4] = {kv[c].x, kv[c].y, kv[c].z, kv[c].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             acc = fma((double)bf16_lo(qa[e]), (double)bf16_lo(ka[e]), acc);
@@ -56,20 +61,23 @@ VLC_DEV void add_below(const ScoreArgs& a, const int4& e) {
 }
 
 // 1: decide each listed entry against K1's row max; undecidable ones (within
-// the row max's own error of the threshold) wait for the exact row max
+// the row max's own error of the threshold) wait for the exact row max.  The
+// exact logit travels in the waiting entry's .w (its weight is always 1).
+template <int D>
 __global__ void fix_flags(ScoreArgs a) {
     const int n = min(a.fix_counts[1], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int4 e = a.flag[i];
         const int64_t rr = (int64_t)e.x * R + e.y;
-        const float x = exact_logit(a, e.x, e.y, e.z) - a.row_max[rr];
+        const float l = exact_logit<D>(a, e.x, e.y, e.z);
+        const float x = l - a.row_max[rr];
         if (x < a.t_star - a.err_max) {
             add_below(a, e);
         } else if (x < a.t_star + a.err_max) {
             const int at = atomicAdd(a.fix_counts, 1);
             if (at < a.cap) {
-                a.cand[at] = e;
+                a.cand[at] = make_int4(e.x, e.y, e.z, __float_as_int(l));
             } else {   // no room: decide against the fp32 row max
                 atomicAdd(a.fix_counts + 2, 1);
                 if (x < a.t_star) add_below(a, e);
@@ -79,21 +87,101 @@ __global__ void fix_flags(ScoreArgs a) {
     }
 }
 
-// 2: exact row max of each listed row, one key per thread (blockIdx.x walks a
-// row's keys, blockIdx.y the listed rows), combined with atomicMax on the
-// order-preserving key
-__global__ void fix_rowscan(ScoreArgs a) {
+// fp64 dot of one bf16 query row and one bf16 key row, sequential (the
+// reference's order)
+template <int D>
+VLC_DEV float exact_dot(const uint4* q, const uint4* k, double inv) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < D / 8; ++c) {
+        const uint4 qv = q[c], kv = k[c];
+        const uint32_t qa[4] = {qv.x, qv.y, qv.z, qv.w}, ka[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            acc = fma((double)bf16_lo(qa[e]), (double)bf16_lo(ka[e]), acc);
+            acc = fma((double)bf16_hi(qa[e]), (double)bf16_hi(ka[e]), acc);
+        }
+    }
+    return (float)(acc * inv);
+}
+
+// 2: exact row max of each listed row (blockIdx.y walks the listed rows,
+// blockIdx.x and the half-warps of a block walk the row's keys), combined with
+// atomicMax on the order-preserving key.  A half-warp reads one key row
+// coalesced (16 lanes x 16 B for D = 128) and forms its float32 dot and
+// sum |q k| by shuffles; only keys whose dot plus the rigorous fp32 error bound
+// ((D + 4) 2^-24 sum |q k|, any summation order) reaches K1's row max minus
+// its error bound get the float64 dot.
+template <int D>
+__global__ void __launch_bounds__(256) fix_rowscan(ScoreArgs a) {
+    constexpr int kLanes = D / 8;                 // lanes per key: 16 B each
+    constexpr int kPerWarp = 32 / kLanes;         // keys per warp and step
+    constexpr float kRel = (float)(D + 4) * 5.9604645e-8f;
     const int nrows = a.fix_counts[3];
     const int64_t R = (int64_t)a.G * a.w;
+    const int lane = threadIdx.x & 31, sub = lane % kLanes, grp = lane / kLanes;
+    const int64_t kslot0 = (int64_t)blockIdx.x * (blockDim.x / 32) * kPerWarp + (threadIdx.x / 32) * kPerWarp + grp;
+    const int64_t kstride = (int64_t)gridDim.x * (blockDim.x / 32) * kPerWarp;
     for (int q = blockIdx.y; q < nrows; q += gridDim.y) {
         const int64_t rr = a.rows[q];
         const int slot = (int)(rr / R), row = (int)(rr % R);
         const int64_t lim = imin(a.n, a.q_base + row % a.w + 1);
+        const float floor_logit = a.row_max[rr] - a.err_max;   // exact max >= this
+        const uint4* qrow = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)slot * R + row) * D);
+        const uint4 qv = qrow[sub];
+        const uint32_t qa[4] = {qv.x, qv.y, qv.z, qv.w};
         float mx = -INFINITY;
-        for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < lim; j += (int64_t)gridDim.x * blockDim.x)
-            mx = fmaxf(mx, exact_logit(a, slot, row, (int)j));
+        constexpr int kU = 4;   // keys per half-warp in flight
+        for (int64_t j0 = kslot0 - grp; j0 < lim; j0 += kU * kstride) {   // warp-uniform trip count
+            uint4 kv[kU];
+            const uint4* krow[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t j = j0 + grp + u * kstride;
+                krow[u] = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) +
+                                                         ((int64_t)slot * a.T + (j < lim ? j : 0)) * D);
+                kv[u] = krow[u][sub];
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int64_t j = j0 + grp + u * kstride;
+                const uint32_t ka[4] = {kv[u].x, kv[u].y, kv[u].z, kv[u].w};
+                float f = 0.f, sa = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float q0 = bf16_lo(qa[e]), q1 = bf16_hi(qa[e]), k0 = bf16_lo(ka[e]), k1 = bf16_hi(ka[e]);
+                    f = fmaf(q1, k1, fmaf(q0, k0, f));
+                    sa = fmaf(fabsf(q1), fabsf(k1), fmaf(fabsf(q0), fabsf(k0), sa));
+                }
+#pragma unroll
+                for (int o = kLanes / 2; o >= 1; o >>= 1) {
+                    f += __shfl_xor_sync(kFull, f, o);
+                    sa += __shfl_xor_sync(kFull, sa, o);
+                }
+                const float hi = (f + 2.f * kRel * sa) * a.inv_scale;
+                if (j < lim && sub == 0 && hi >= floor_logit - fabsf(floor_logit) * 1e-6f) {
+                    // list it (the flag list is free once fix_flags ran); scored in parallel next
+                    const int at = atomicAdd(a.fix_counts + 4, 1);
+                    if (at < a.cap) a.flag[at] = make_int4(slot, row, (int)j, 0);
+                    else mx = fmaxf(mx, exact_dot<D>(qrow, krow[u], a.inv_scale_d));
+                }
+            }
+        }
         mx = warp_max(mx);
-        if ((threadIdx.x & 31) == 0 && mx != -INFINITY) atomicMax(a.rmax_key + rr, fkey(mx));
+        if (lane == 0 && mx != -INFINITY) atomicMax(a.rmax_key + rr, fkey(mx));
+    }
+}
+
+// 2b: the row scan's candidates, one float64 dot per thread
+template <int D>
+__global__ void fix_rowmax(ScoreArgs a) {
+    const int n = min(a.fix_counts[4], a.cap);
+    const int64_t R = (int64_t)a.G * a.w;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int4 e = a.flag[i];
+        const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)e.x * R + e.y) * D);
+        const uint4* k = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) + ((int64_t)e.x * a.T + e.z) * D);
+        atomicMax(a.rmax_key + (int64_t)e.x * R + e.y, fkey(exact_dot<D>(q, k, a.inv_scale_d)));
     }
 }
 
@@ -105,12 +193,21 @@ __global__ void fix_deferred(ScoreArgs a) {
     const int stride = gridDim.x * blockDim.x;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const int4 e = a.cand[i];
-        if (exact_logit(a, e.x, e.y, e.z) - funkey(a.rmax_key[(int64_t)e.x * R + e.y]) < a.t_star) add_below(a, e);
+        if (__int_as_float(e.w) - funkey(a.rmax_key[(int64_t)e.x * R + e.y]) < a.t_star)
+            add_below(a, make_int4(e.x, e.y, e.z, 1));
     }
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.fix_counts[3]; q += stride) {
         const int64_t rr = a.rows[q];
         a.row_max[rr] = funkey(a.rmax_key[rr]);
     }
+}
+
+template <int D>
+void launch_fixups(const ScoreArgs& a, cudaStream_t st) {
+    fix_flags<D><<<296, 256, 0, st>>>(a);
+    fix_rowscan<D><<<dim3(24, 148), 256, 0, st>>>(a);
+    fix_rowmax<D><<<296, 256, 0, st>>>(a);
+    fix_deferred<<<148, 256, 0, st>>>(a);
 }
 
 }  // namespace
@@ -132,15 +229,14 @@ cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st) {
         if (e != cudaSuccess) return e;
     }
     if (a.cap > 0) {
-        e = cudaMemsetAsync(a.fix_counts, 0, 4 * sizeof(int), st);
+        e = cudaMemsetAsync(a.fix_counts, 0, 8 * sizeof(int), st);
         if (e == cudaSuccess) e = cudaMemsetAsync(a.rmax_key, 0, sizeof(unsigned) * a.slots * a.G * a.w, st);
         if (e != cudaSuccess) return e;
     }
     e = launch_score_stats_tc(a, score_partials((int64_t)a.G * a.w), st);
     if (e != cudaSuccess || a.cap <= 0) return e;
-    fix_flags<<<296, 256, 0, st>>>(a);
-    fix_rowscan<<<dim3(16, 148), 256, 0, st>>>(a);
-    fix_deferred<<<148, 256, 0, st>>>(a);
+    if (a.d == 64) launch_fixups<64>(a, st);
+    else launch_fixups<128>(a, st);
     return cudaGetLastError();
 }
 
