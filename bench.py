@@ -124,7 +124,8 @@ class ClockSampler:
                 pass
             time.sleep(0.02)
 
-    def __enter__(self):
+    def __enter__(self):   # re-entrant: one sampler covers several timed regions
+        self.stop.clear()
         if self.nv is not None:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
@@ -347,16 +348,19 @@ def run_gpu_arm(args):
     e_kp, e_vp = hp(ks[:, :, :, :m]), hp(vs[:, :, :, :m])
     e_kd, e_vd = hp(ks[:, :, :, m:m + n_dec]), hp(vs[:, :, :, m:m + n_dec])
     e2e_ms, h2d, d2h = [], 0, 0
-    for i in range(max(3, args.warmup) + args.steps):
-        flush.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(st)
-        h_counts, h_out, copied = eng.run_from_host(e_qw, e_kp, e_vp, e_qd, e_kd, e_vd)
-        b.record(st)
-        torch.cuda.synchronize()
-        h2d = copied + eng.zero_copy_bytes(h_counts)
-        d2h = h_counts.numel() * 8 + h_out.numel() * 4
-        if i >= max(3, args.warmup):
+    for i in range(max(3, args.warmup)):   # warm-up (untimed, unsampled)
+        eng.run_from_host(e_qw, e_kp, e_vp, e_qd, e_kd, e_vd)
+    torch.cuda.synchronize()
+    with clk:   # the e2e timed region is sampled too
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            h_counts, h_out, copied = eng.run_from_host(e_qw, e_kp, e_vp, e_qd, e_kd, e_vd)
+            b.record(st)
+            torch.cuda.synchronize()
+            h2d = copied + eng.zero_copy_bytes(h_counts)
+            d2h = h_counts.numel() * 8 + h_out.numel() * 4
             e2e_ms.append(a.elapsed_time(b))
     t_e2e = torch.tensor([float(np.mean(e2e_ms))], device="cuda")
     if world > 1:
