@@ -164,6 +164,23 @@ VLC_API int vlc_copy_2d(void *dst, int64_t dpitch, const void *src, int64_t spit
                     int64_t height, void *stream);
 
 /*
+ * Prefill: causal attention of the m prompt rows
+ * of every query head, out[s, r] = softmax_j<=r(q_r . k_j * scale) V (reference
+ * bench.py:196-234 _prefill_layer), on tcgen05, plus the exact per-row softmax
+ * statistics the compression path needs (row_max in logit units as K1's, row_sum
+ * = sum exp(l - max); NULL to skip).  q: bf16 [B*L*Hq, q_rows, d]; k, v: bf16
+ * [B*L*Hkv, kv_rows, d] (q_rows, kv_rows >= m); head_dim in {64, 128}.  P is
+ * rounded to bf16 for the P V product (relative error ~2^-9 per weight, as
+ * every tensor-core attention).  out: f32 [B*L*Hq, m, d].  ws: device
+ * workspace of vlc_prefill_ws_bytes() bytes (V^T), 256-byte aligned.
+ */
+VLC_API int64_t vlc_prefill_ws_bytes(int32_t kv_slots, int32_t head_dim, int64_t prompt_len);
+VLC_API int vlc_prefill(const void *q, int64_t q_rows, const void *k, const void *v, int64_t kv_rows,
+                    int32_t batch, int32_t layers, int32_t q_heads, int32_t kv_heads, int32_t head_dim,
+                    int64_t prompt_len, double scale, void *ws, int64_t ws_bytes, float *out,
+                    float *row_max, float *row_sum, void *stream);
+
+/*
  * Analysis rows.  Dense causal softmax of fp32
  * query rows against fp32 keys: row r (absolute query first_row + r) of head h
  * sees keys [0, min(key_limit, first_row + r + 1)) of KV head h / group;

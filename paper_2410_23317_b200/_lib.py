@@ -42,6 +42,9 @@ _SIGNATURES = {
     "vlc_copy_2d": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "vlc_decode_step": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _I32,
                                        _I32, _I32, _I32, _I32, _F64, _I32, _P, _P]),
+    "vlc_prefill_ws_bytes": (_I64, [_I32, _I32, _I64]),
+    "vlc_prefill": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _I32, _I32, _I32, _I32, _I32, _I64, _F64, _P, _I64,
+                                   _P, _P, _P, _P]),
     "vlc_attention_rows": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _I64, _P,
                                           _F64, _I64, _I64, _I64, _P, _P]),
 }

@@ -1,0 +1,324 @@
+// prefill.cu -- f2: causal prefill attention over the prompt on tcgen05, with
+// the per-row softmax statistics (row max, row sum) as a by-product.
+//
+// reference: bench.py:196-234 (_prefill_layer: causal softmax(Q K^T / sqrt(d)) V
+// over the m prompt rows of every head, float32) -- the step before the
+// compression path; PAPER.md:528-553 (the post-vision statistics ride on the
+// prefill's Q K^T).
+//
+// Two passes per CTA = (query head, block of 128 prompt rows), like K1:
+//   pass 1: S = Q K^T tile by tile (TMEM) -> exact row max / sum (thread = row)
+//   pass 2: S again -> P = 2^(S c1 - max c1) / sum as bf16 into shared memory
+//           (the UMMA A layout, 128-byte swizzle) -> O += P V^T^T on tcgen05
+//           with V^T tiles (pre-transposed once, K-major) as the B operand.
+// The row max is final before any P is formed, so O accumulates in TMEM with
+// no rescaling; the cost is one extra Q K^T (3 MMAs per tile instead of 2).
+// Warps: 0 K producer, 1 MMA issuer, 2 TMEM allocator, 3 V^T producer,
+// 4-19 epilogue (lane quarter x 32-column group).
+#include <cuda.h>
+
+#include "sm100.cuh"
+#include "vlc_common.cuh"
+#include "vlc_kernels.h"
+
+namespace vlc {
+namespace {
+
+constexpr int kM = 128;          // rows per CTA
+constexpr int kN = 128;          // keys per tile
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr uint32_t kTmemCols = 512;   // S: 2 x 128, O: d <= 128
+
+template <int D>
+struct PL {
+    static constexpr int KB = D / 64;
+    static constexpr uint32_t kQ = KB * kM * 128;        // Q block
+    static constexpr uint32_t kK = KB * kN * 128;        // one K tile
+    static constexpr uint32_t kV = 2 * D * 128;          // one V^T tile: D rows x 128 keys
+    static constexpr uint32_t kP = 2 * kM * 128;         // P: 128 rows x 128 keys
+    static constexpr uint32_t kBytes = kQ + 2 * kK + 2 * kV + kP + 1024;
+};
+
+VLC_DEV uint32_t pack_bf16(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// byte offset of 16-byte chunk c (8 bf16) of row r in a 128B-swizzled tile of
+// `rows` rows (64-element boxes, `rows` x 128 B each) -- the TMA / UMMA layout
+VLC_DEV uint32_t swz(int rows, int r, int c) {
+    return (uint32_t)((c >> 3) * rows * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+               const __grid_constant__ CUtensorMap vmap, PrefillArgs a) {
+    using LY = PL<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sq = smem;
+    uint8_t* sk = sq + LY::kQ;
+    uint8_t* sv = sk + 2 * LY::kK;
+    uint8_t* sp = sv + 2 * LY::kV;
+    __shared__ uint64_t qfull, kfull[2], kempty[2], vfull[2], vempty[2], tfull[2], tempty[2], pfull, pempty, ofull;
+    __shared__ uint32_t tmem_slot;
+    __shared__ float2 rowstat[4 * kM];
+    __shared__ float c_mb[kM], c_il[kM];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sq_slot = blockIdx.y;                                  // (b, l, query head)
+    const int rb = gridDim.x - 1 - blockIdx.x;                       // longest blocks first
+    const int64_t kv_slot = (int64_t)(sq_slot / a.Hq) * a.Hkv + (sq_slot % a.Hq) / (a.Hq / a.Hkv);
+    const int64_t r0 = (int64_t)rb * kM;
+    const int64_t key_end = imin(a.m, r0 + kM);                      // keys any row here sees
+    const int T = (int)((key_end + kN - 1) / kN);
+
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&qfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            sm100::mbar_init(kfull + i, 1); sm100::mbar_init(kempty + i, 1);
+            sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1);
+            sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kEpiWarps);
+        }
+        sm100::mbar_init(&pfull, kEpiWarps);
+        sm100::mbar_init(&pempty, 1);
+        sm100::mbar_init(&ofull, 1);
+        sm100::fence_barrier_init();
+    }
+    if (warp == 2) sm100::tmem_alloc(&tmem_slot, kTmemCols);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t tmem_o = tmem + 2 * kN;
+
+    if (warp < 4) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n");
+        if (warp == 0 && lane == 0) {
+            // ---- Q once, then the K tiles twice (pass 1, pass 2)
+            sm100::tma_prefetch(&qmap);
+            sm100::tma_prefetch(&kmap);
+            sm100::mbar_expect_tx(&qfull, LY::kQ);
+            for (int kb = 0; kb < LY::KB; ++kb)
+                sm100::tma_load_2d(sq + kb * kM * 128, &qmap, &qfull, kb * 64, (int)(sq_slot * a.q_rows + r0));
+            for (int it = 0; it < 2 * T; ++it) {
+                const int st = it & 1, t = it < T ? it : it - T;
+                sm100::mbar_wait(kempty + st, ((it >> 1) & 1) ^ 1);
+                sm100::mbar_expect_tx(kfull + st, LY::kK);
+                for (int kb = 0; kb < LY::KB; ++kb)
+                    sm100::tma_load_2d(sk + st * LY::kK + kb * kN * 128, &kmap, kfull + st, kb * 64,
+                                       (int)(kv_slot * a.kv_rows + (int64_t)t * kN));
+            }
+        } else if (warp == 3 && lane == 0) {
+            // ---- V^T tiles (pass 2): D rows (dims) x 128 keys
+            sm100::tma_prefetch(&vmap);
+            for (int t = 0; t < T; ++t) {
+                const int st = t & 1;
+                sm100::mbar_wait(vempty + st, ((t >> 1) & 1) ^ 1);
+                sm100::mbar_expect_tx(vfull + st, LY::kV);
+                for (int kb = 0; kb < 2; ++kb)
+                    sm100::tma_load_2d(sv + st * LY::kV + kb * D * 128, &vmap, vfull + st, t * kN + kb * 64,
+                                       (int)(kv_slot * D));
+            }
+        } else if (warp == 1 && lane == 0) {
+            // ---- MMA issuer
+            constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kM, kN);
+            constexpr uint32_t idesc_o = sm100::idesc_bf16_f32(kM, D);
+            const uint32_t q_addr = sm100::smem_u32(sq), p_addr = sm100::smem_u32(sp);
+            auto qk = [&](int it) {   // S[it & 1] = Q K^T of the K tile in ring stage it & 1
+                const int st = it & 1;
+                sm100::mbar_wait(tempty + st, ((it >> 1) & 1) ^ 1);
+                sm100::mbar_wait(kfull + st, (it >> 1) & 1);
+                sm100::tc_fence_after();
+                const uint32_t k_addr = sm100::smem_u32(sk + st * LY::kK);
+#pragma unroll
+                for (int kb = 0; kb < LY::KB; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        sm100::mma_bf16(tmem + st * kN, sm100::sdesc_k_sw128(q_addr + kb * kM * 128 + kk * 32),
+                                        sm100::sdesc_k_sw128(k_addr + kb * kN * 128 + kk * 32), idesc_s,
+                                        (kb | kk) != 0);
+                sm100::mma_commit(kempty + st);
+                sm100::mma_commit(tfull + st);
+            };
+            auto pv = [&](int t) {    // O += P V for key tile t
+                const int st = t & 1;
+                sm100::mbar_wait(&pfull, t & 1);
+                sm100::mbar_wait(vfull + st, (t >> 1) & 1);
+                sm100::tc_fence_after();
+                const uint32_t v_addr = sm100::smem_u32(sv + st * LY::kV);
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        sm100::mma_bf16(tmem_o, sm100::sdesc_k_sw128(p_addr + kb * kM * 128 + kk * 32),
+                                        sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32), idesc_o,
+                                        (t | kb | kk) != 0);
+                sm100::mma_commit(&pempty);
+                sm100::mma_commit(vempty + st);
+            };
+            sm100::mbar_wait(&qfull, 0);
+            for (int it = 0; it < T; ++it) qk(it);
+            for (int t = 0; t < T; ++t) {
+                qk(T + t);
+                if (t > 0) pv(t - 1);
+            }
+            pv(T - 1);
+            sm100::mma_commit(&ofull);
+        }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
+        // ---- epilogue: warp -> (TMEM lane quarter `sub`, 32-column group `cg`)
+        const int ew = warp - 4, sub = warp & 3, cg = ew >> 2;
+        const int li = 32 * sub + lane;                               // row within the block
+        const int64_t r = r0 + li;
+        const bool row_ok = r < a.m;
+        const int64_t row_end = row_ok ? r + 1 : 0;                   // causal: keys [0, r]
+        const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + cg * 32;
+        const float c1 = a.inv_scale * kLog2e;
+        float l[32];
+
+        // pass 1: running max of the raw dots and rescaled sum of 2^(.)
+        float m = -INFINITY, sum = 0.f;
+        for (int it = 0; it < T; ++it) {
+            const int st = it & 1;
+            sm100::mbar_wait(tfull + st, (it >> 1) & 1);
+            sm100::tc_fence_after();
+            sm100::tmem_ld32(lane_addr + st * kN, l);
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tempty + st);
+            const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
+            float cmax = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+            if (cmax > m) {
+                sum *= ex2((m - cmax) * c1);
+                m = cmax;
+            }
+            const float mb = m * c1;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 32; ++k) acc[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+            sum += (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+        rowstat[cg * kM + li] = make_float2(m, sum);
+        sm100::named_bar_sync(1, kEpiWarps * 32);
+        if (cg == 0) {
+            float M = -INFINITY, S = 0.f;
+#pragma unroll
+            for (int g = 0; g < 4; ++g) M = fmaxf(M, rowstat[g * kM + li].x);
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                const float2 h = rowstat[g * kM + li];
+                if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
+            }
+            c_mb[li] = row_ok ? M * c1 : 0.f;
+            c_il[li] = row_ok ? 1.f / S : 0.f;
+            if (row_ok && a.row_max) {
+                a.row_max[(int64_t)sq_slot * a.m + r] = M * a.inv_scale;
+                a.row_sum[(int64_t)sq_slot * a.m + r] = S;
+            }
+        }
+        sm100::named_bar_sync(1, kEpiWarps * 32);
+        const float mb = c_mb[li], il = c_il[li];
+
+        // pass 2: P = 2^(l c1 - mb) / S (0 past the causal frontier) as bf16 into
+        // the A-operand layout, then the MMA warp adds P V into O
+        for (int t = 0; t < T; ++t) {
+            const int it = T + t, st = it & 1;
+            sm100::mbar_wait(tfull + st, (it >> 1) & 1);
+            sm100::tc_fence_after();
+            sm100::tmem_ld32(lane_addr + st * kN, l);
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(tempty + st);
+            const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
+            uint32_t pk[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) * il : 0.f;
+                const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) * il : 0.f;
+                pk[k] = pack_bf16(p0, p1);
+            }
+            sm100::mbar_wait(&pempty, (t & 1) ^ 1);                   // the previous P V has read P
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                *reinterpret_cast<uint4*>(sp + swz(kM, li, cg * 4 + q)) =
+                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            sm100::fence_proxy_async();                              // generic writes -> async proxy
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&pfull);
+        }
+
+        // O: thread = row, warp cg holds dims 32 cg .. 32 cg + 31
+        sm100::mbar_wait(&ofull, 0);
+        sm100::tc_fence_after();
+        if (cg * 32 < D) {
+            sm100::tmem_ld32(tmem_o + (uint32_t(32 * sub) << 16) + cg * 32, l);
+            if (row_ok) {
+                float4* dst = reinterpret_cast<float4*>(a.out + ((int64_t)sq_slot * a.m + r) * D + cg * 32);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) dst[q] = make_float4(l[4 * q], l[4 * q + 1], l[4 * q + 2], l[4 * q + 3]);
+            }
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, kTmemCols);
+    }
+}
+
+// V [slots, kv_rows, D] -> V^T [slots, D, tpad] (keys contiguous), zero past m
+__global__ void transpose_v(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int64_t kv_rows,
+                            int d, int64_t m, int64_t tpad) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int64_t s = blockIdx.z;
+    const int64_t j0 = (int64_t)blockIdx.x * 32, d0 = (int64_t)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t j = j0 + i, dd = d0 + threadIdx.x;
+        tile[i][threadIdx.x] = (j < m && dd < d) ? v[(s * kv_rows + j) * d + dd] : __float2bfloat16(0.f);
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t dd = d0 + i, j = j0 + threadIdx.x;
+        if (dd < d && j < tpad) vt[(s * d + dd) * tpad + j] = tile[threadIdx.x][i];
+    }
+}
+
+template <int D>
+cudaError_t launch_prefill_d(const PrefillArgs& a, cudaStream_t st) {
+    const int64_t tpad = prefill_tpad(a.m);
+    const int64_t kv_slots = (int64_t)a.B * a.L * a.Hkv;
+    dim3 tg((unsigned)((tpad + 31) / 32), (unsigned)((D + 31) / 32), (unsigned)kv_slots);
+    transpose_v<<<tg, dim3(32, 8), 0, st>>>(static_cast<const __nv_bfloat16*>(a.v), static_cast<__nv_bfloat16*>(a.vt),
+                                           a.kv_rows, D, a.m, tpad);
+    CUtensorMap qmap, kmap, vmap;
+    const int64_t q_slots = (int64_t)a.B * a.L * a.Hq;
+    if (!make_tmap_2d(&qmap, a.q, q_slots * a.q_rows, D, kM)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d(&kmap, a.k, kv_slots * a.kv_rows, D, kN)) return cudaErrorInvalidValue;
+    if (!make_tmap_2d_strided(&vmap, a.vt, kv_slots * D, (int)tpad, tpad, D, true)) return cudaErrorInvalidValue;
+    const size_t smem = PL<D>::kBytes;
+    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((a.m + kM - 1) / kM), (unsigned)q_slots);
+    prefill_kernel<D><<<grid, kThreads, smem, st>>>(qmap, kmap, vmap, a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int64_t prefill_tpad(int64_t m) { return (m + 127) / 128 * 128; }
+
+cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st) {
+    if (a.d == 64) return launch_prefill_d<64>(a, st);
+    if (a.d == 128) return launch_prefill_d<128>(a, st);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace vlc

@@ -218,6 +218,32 @@ int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head
     return cuda_status(vlc::launch_gather(a, (cudaStream_t)stream), "gather");
 }
 
+int64_t vlc_prefill_ws_bytes(int32_t kv_slots, int32_t head_dim, int64_t prompt_len) {
+    return (int64_t)kv_slots * head_dim * vlc::prefill_tpad(prompt_len) * 2;
+}
+
+int vlc_prefill(const void* q, int64_t q_rows, const void* k, const void* v, int64_t kv_rows, int32_t batch,
+                int32_t layers, int32_t q_heads, int32_t kv_heads, int32_t head_dim, int64_t prompt_len, double scale,
+                void* ws, int64_t ws_bytes, float* out, float* row_max, float* row_sum, void* stream) {
+    if (!q || !k || !v || !ws || !out) return fail(VLC_EINVAL, "prefill: null pointer");
+    if ((row_max == nullptr) != (row_sum == nullptr)) return fail(VLC_EINVAL, "prefill: row_max and row_sum go together");
+    if (batch < 1 || layers < 1 || q_heads < 1 || kv_heads < 1 || q_heads % kv_heads || prompt_len < 1)
+        return fail(VLC_EINVAL, "prefill: bad shape");
+    if (head_dim != 64 && head_dim != 128) return fail(VLC_EUNSUPPORTED, "head_dim: %d not in {64, 128}", head_dim);
+    if (q_rows < prompt_len || kv_rows < prompt_len) return fail(VLC_EINVAL, "prefill: q_rows / kv_rows < prompt_len");
+    const int64_t need = vlc_prefill_ws_bytes(batch * layers * kv_heads, head_dim, prompt_len);
+    if (ws_bytes < need || (reinterpret_cast<uintptr_t>(ws) & 255))
+        return fail(VLC_EINVAL, "prefill: ws must be 256-byte aligned with %lld bytes", (long long)need);
+    if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(k) | reinterpret_cast<uintptr_t>(out)) & 15)
+        return fail(VLC_EINVAL, "prefill: q / k / out must be 16-byte aligned");
+    if (!(scale > 0.0)) return fail(VLC_EINVAL, "scale: must be > 0");
+    vlc::PrefillArgs a{};
+    a.q = q; a.k = k; a.v = v; a.vt = ws; a.q_rows = q_rows; a.kv_rows = kv_rows; a.m = prompt_len;
+    a.B = batch; a.L = layers; a.Hq = q_heads; a.Hkv = kv_heads; a.d = head_dim; a.inv_scale = (float)scale;
+    a.out = out; a.row_max = row_max; a.row_sum = row_sum;
+    return cuda_status(vlc::launch_prefill(a, (cudaStream_t)stream), "prefill");
+}
+
 int vlc_attention_rows(const float* q, const float* k, int32_t heads, int32_t group, int32_t head_dim,
                        int64_t rows, int64_t key_rows, int64_t first_row, int64_t key_limit, int64_t out_cols,
                        double* probs, double filter_p, int64_t prompt_len, int64_t vision_start,

@@ -127,6 +127,22 @@ struct DecodeArgs {
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 
+// f2: causal prefill attention over the prompt (prefill.cu).
+struct PrefillArgs {
+    const void* q;             // bf16 [B*L*Hq, q_rows, d] (prompt rows first)
+    const void* k;             // bf16 [B*L*Hkv, kv_rows, d]
+    const void* v;
+    void* vt;                  // workspace: bf16 V^T [B*L*Hkv, d, prefill_tpad(m)]
+    int64_t q_rows, kv_rows, m;
+    int B, L, Hq, Hkv, d;
+    float inv_scale;
+    float* out;                // f32 [B*L*Hq, m, d]
+    float* row_max;            // f32 [B*L*Hq, m] (logit units) or null
+    float* row_sum;            // f32 [B*L*Hq, m] (sum of exp(l - max)) or null
+};
+int64_t prefill_tpad(int64_t m);
+cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st);
+
 // f4 analysis: dense causal softmax rows over fp32 trace rows (eval_rows.cu).
 struct RowsArgs {
     const float* q;            // f32 [heads, rows, d]: query rows first_row .. first_row+rows-1

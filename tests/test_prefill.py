@@ -1,0 +1,85 @@
+"""Row f2 (prefill attention): oracle restatement and the B200 kernel against
+the reference's own bench._prefill_layer (tests/golden/make_prefill_golden.py).
+
+The oracle (float32 numpy, same tiling) must match the reference bit for bit.
+The device kernel forms P in bf16 for the P V product (as every tensor-core
+attention): outputs agree to 2e-2 absolute on unit-variance values (|P| error
+<= 2^-9 relative per weight); the row statistics it emits equal K1's.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2410_23317_b200.trace import round_to_bf16
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+from make_prefill_golden import CASES, inputs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def pg():
+    return np.load(os.path.join(HERE, "golden", "prefill_golden.npz"))
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_oracle_prefill_matches_reference(pg, case):
+    seed, h, hkv, d, m, tile = case
+    q, k, v = inputs(seed, h, hkv, d, m, round_to_bf16)
+    np.testing.assert_array_equal(O.prefill_layer(q, k, v, m, tile), pg[f"c{seed}_out"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", CASES)
+def test_gpu_prefill_matches_reference(pg, case):
+    from paper_2410_23317_b200.prefill import prefill_attention
+
+    seed, h, hkv, d, m, tile = case
+    q, k, v = inputs(seed, h, hkv, d, m, round_to_bf16)
+    got = prefill_attention(q, k, v, m, tile)
+    want = pg[f"c{seed}_out"]
+    assert got.shape == want.shape and np.isfinite(got).all()
+    np.testing.assert_allclose(got, want, atol=2e-2, rtol=0)
+    assert np.abs(got - want).mean() < 2e-3
+
+
+@pytest.mark.gpu
+def test_gpu_prefill_stats_equal_k1():
+    """The prefill's row max equals K1's for the window rows (same tensor-core
+    dots); row sums agree to float32 rounding of a different partial order."""
+    import torch
+
+    from paper_2410_23317_b200.engine import Shape, VLCache
+    from paper_2410_23317_b200.prefill import prefill
+
+    B, L, HQ, HKV, D, M, W = 1, 2, 8, 2, 128, 700, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q = (torch.randn((B, L, HQ, M, D), device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    k = torch.randn((B, L, HKV, M, D), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((B, L, HKV, M, D), device="cuda", generator=g).to(torch.bfloat16)
+    _, rmax, rsum = prefill(q, k, v, M)
+    eng = VLCache(Shape(B, L, HQ, HKV, D, M, W), exact=False)
+    eng.score_stats(q[:, :, :, M - W:].contiguous(), k)
+    torch.cuda.synchronize()
+    k1_max = eng.row_max.view(B, L, HQ, W)
+    k1_sum = eng.row_sum.view(B, L, HQ, W)
+    assert torch.equal(rmax[..., M - W:], k1_max)
+    torch.testing.assert_close(rsum[..., M - W:], k1_sum, rtol=2e-6, atol=0)
+
+
+@pytest.mark.gpu
+def test_gpu_prefill_validation():
+    import torch
+
+    from paper_2410_23317_b200 import ValidationError
+    from paper_2410_23317_b200.prefill import prefill
+
+    q = torch.zeros((1, 1, 2, 16, 96), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(Exception, match="head_dim"):
+        prefill(q, q[:, :, :1].contiguous(), q[:, :, :1].contiguous(), 16)
+    q = torch.zeros((1, 1, 2, 16, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValidationError, match="m: must be"):
+        prefill(q, q, q, 17)
