@@ -69,14 +69,15 @@ def ncu_traffic(kernel):
     return data[kernel]["bytes"], os.path.relpath(files[-1], ROOT)
 
 
-def synth_inputs(batch, seed0, w):
-    """bf16-rounded host arrays [B, L, H, rows, d] from the reference generator."""
+def synth_inputs(batch, seed0, w, layers=None):
+    """bf16-rounded host arrays [B, L, H, rows, d] from the reference generator
+    (q_win holds the last w prompt rows; w = prompt_len keeps them all)."""
     from paper_2410_23317_b200.trace import GenSpec, iter_layers, round_to_bf16, synthesize_values
 
     c = CFG
     qw, qd, ks, vs = [], [], [], []
     for b in range(batch):
-        spec = GenSpec(num_layers=c["layers"], num_query_heads=c["q_heads"], num_kv_heads=c["kv_heads"],
+        spec = GenSpec(num_layers=layers or c["layers"], num_query_heads=c["q_heads"], num_kv_heads=c["kv_heads"],
                        head_dim=c["head_dim"], prompt_len=c["prompt_len"], post_vision_len=c["tau"],
                        decode_len=c["n_out"] - 1, seed=seed0 + b)
         k_l, qw_l, qd_l = [], [], []

@@ -83,6 +83,18 @@ VLC_API int vlc_score_stats(const void *q_win, const void *keys, int32_t slots, 
                     void *exact_ws, int64_t exact_ws_bytes, void *stream);
 
 /*
+ * K1 riding on the prefill (row f2): as vlc_score_stats, but the window rows'
+ * softmax statistics come from vlc_prefill (stat_max in logit units, stat_sum;
+ * [B*L*Hq, stat_ld] with the window at columns q_base .. q_base + window - 1),
+ * so K1 runs its column pass only.  row_max / row_sum echo the given values.
+ */
+VLC_API int vlc_score_stats_given(const void *q_win, const void *keys, int32_t slots, int32_t group,
+                    int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window, int64_t q_base,
+                    double p, double scale, const float *stat_max, const float *stat_sum, int64_t stat_ld,
+                    float *row_max, float *row_sum, float *col_partial, uint64_t *below_head,
+                    int32_t *below_col, void *exact_ws, int64_t exact_ws_bytes, void *stream);
+
+/*
  * K2 allocate.  gamma[b,l,h] = below/causal (reference sparsity.py:79),
  * gamma_mean = mean over heads (sparsity.py:41-43), then
  * allocate_sparsity_aware (budget.py:86-111): bit-identical to numpy given

@@ -32,6 +32,8 @@ _SIGNATURES = {
     "vlc_score_exact_bytes": (_I64, [_I32, _I32, _I64, _I64]),
     "vlc_score_stats": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64,
                                        _F64, _P, _P, _P, _P, _P, _P, _I64, _P]),
+    "vlc_score_stats_given": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64, _F64,
+                                             _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64, _P]),
     "vlc_allocate": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _F64, _F64,
                                     _F64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "vlc_allocate_from_gamma": (ctypes.c_int, [_P, _I32, _I32, _I32, _I64, _F64, _F64, _F64, _I64,

@@ -104,7 +104,8 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const int64_t i_max = (r_last / a.w == r_first / a.w) ? r_last % a.w : a.w - 1;
     const int64_t blk_end = imin(a.n, a.q_base + i_max + 1);   // keys any row here can see
     const int T = (int)((blk_end + kN - 1) / kN);
-    const int iters = 2 * T;
+    const int P1 = a.stat_max ? 0 : T;    // pass-1 tiles (none when the row statistics are given)
+    const int iters = P1 + T;
     const int64_t head0 = r_first / a.w;
 
     if (threadIdx.x == 0) {
@@ -135,7 +136,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             for (int it = 0; it < iters; ++it) {
                 const int st = it % kStages;
                 const uint32_t ph = (it / kStages) & 1;
-                const int t = it < T ? it : it - T;
+                const int t = it < P1 ? it : it - P1;
                 sm100::mbar_wait(empty + st, ph ^ 1);
                 sm100::mbar_expect_tx(full + st, LY::kKBytes);
                 uint8_t* kdst = smem + LY::kQBytes + st * LY::kKBytes;
@@ -159,7 +160,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 sm100::mbar_wait(full + st, ph);
                 sm100::tc_fence_after();
                 const uint32_t k_addr = sm100::smem_u32(smem + LY::kQBytes + st * LY::kKBytes);
-                const bool rows_on_lanes = it < T;
+                const bool rows_on_lanes = it < P1;
 #pragma unroll
                 for (int kb = 0; kb < LY::KB; ++kb) {
 #pragma unroll
@@ -194,7 +195,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int64_t i = row_ok ? r % a.w : 0;
             const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
             float m = -INFINITY, sum = 0.f;
-            for (int it = set; it < T; it += 2) {
+            for (int it = set; it < P1; it += 2) {
                 const int acc = it % kAcc;
                 sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
                 sm100::tc_fence_after();
@@ -235,19 +236,27 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             rowstat[(set * 2 + half) * kM + lane_idx] = make_float2(m, sum);
             sm100::named_bar_sync(1, kEpiWarps * 32);
             if (ew < 4) {
-                float M = -INFINITY;
+                float M = -INFINITY, S = 0.f, mb, rm;
+                if (a.stat_max) {   // given (logit units): mb = max * log2e
+                    const int64_t gi = ((int64_t)s * a.G + r / a.w) * a.stat_ld + a.stat_row0 + i;
+                    rm = row_ok ? a.stat_max[gi] : 0.f;
+                    S = row_ok ? a.stat_sum[gi] : 1.f;
+                    mb = rm * kLog2e;
+                } else {
 #pragma unroll
-                for (int g4 = 0; g4 < 4; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
-                float S = 0.f;
+                    for (int g4 = 0; g4 < 4; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
 #pragma unroll
-                for (int g4 = 0; g4 < 4; ++g4) {
-                    const float2 h = rowstat[g4 * kM + lane_idx];
-                    if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
+                    for (int g4 = 0; g4 < 4; ++g4) {
+                        const float2 h = rowstat[g4 * kM + lane_idx];
+                        if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
+                    }
+                    mb = M * c1;
+                    rm = M * a.inv_scale;
                 }
                 if (row_ok) {
-                    a.row_max[(int64_t)s * R + r] = M * a.inv_scale;
+                    a.row_max[(int64_t)s * R + r] = rm;
                     a.row_sum[(int64_t)s * R + r] = S;
-                    c_mb[lane_idx] = M * c1;
+                    c_mb[lane_idx] = mb;
                     c_is[lane_idx] = 1.f / S;
                     c_t2[lane_idx] = a.t_star * kLog2e;
                     c_lim[lane_idx] = (int)(a.q_base + i);
@@ -270,8 +279,8 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const int64_t rg = r_first + r0;
         const bool one_head = rg / a.w == (rg + 63) / a.w;
         float* colp = a.col_partial + ((int64_t)s * nparts + rb * 2 + half) * a.n;
-        for (int it = T + ((T ^ set) & 1); it < iters; it += 2) {
-            const int t = it - T;
+        for (int it = P1 + ((P1 ^ set) & 1); it < iters; it += 2) {
+            const int t = it - P1;
             const int j = t * kN + lane_idx;                     // this thread's key
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
             const int acc = it % kAcc;

@@ -76,11 +76,42 @@ int64_t vlc_score_exact_bytes(int32_t slots, int32_t group, int64_t window, int6
     return vlc::exact_ws_bytes(slots, (int64_t)group * window, entries);
 }
 
+static int score_stats_impl(const void* q_win, const void* keys, int32_t slots, int32_t group,
+                            int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
+                            int64_t q_base, double p, double scale, const float* stat_max, const float* stat_sum,
+                            int64_t stat_ld, int64_t stat_row0, float* row_max, float* row_sum, float* col_partial,
+                            uint64_t* below_head, int32_t* below_col, void* exact_ws, int64_t exact_ws_bytes,
+                            void* stream);
+
 int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t group,
                     int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
                     int64_t q_base, double p, double scale, float* row_max, float* row_sum, float* col_partial,
                     uint64_t* below_head, int32_t* below_col, void* exact_ws, int64_t exact_ws_bytes,
                     void* stream) {
+    return score_stats_impl(q_win, keys, slots, group, head_dim, key_rows, n_keys, window, q_base, p, scale,
+                            nullptr, nullptr, 0, 0, row_max, row_sum, col_partial, below_head, below_col,
+                            exact_ws, exact_ws_bytes, stream);
+}
+
+int vlc_score_stats_given(const void* q_win, const void* keys, int32_t slots, int32_t group,
+                          int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
+                          int64_t q_base, double p, double scale, const float* stat_max, const float* stat_sum,
+                          int64_t stat_ld, float* row_max, float* row_sum, float* col_partial,
+                          uint64_t* below_head, int32_t* below_col, void* exact_ws, int64_t exact_ws_bytes,
+                          void* stream) {
+    if (!stat_max || !stat_sum) return fail(VLC_EINVAL, "score_stats_given: null statistics");
+    if (stat_ld < q_base + window) return fail(VLC_EINVAL, "score_stats_given: stat_ld < q_base + window");
+    return score_stats_impl(q_win, keys, slots, group, head_dim, key_rows, n_keys, window, q_base, p, scale,
+                            stat_max, stat_sum, stat_ld, q_base, row_max, row_sum, col_partial, below_head,
+                            below_col, exact_ws, exact_ws_bytes, stream);
+}
+
+static int score_stats_impl(const void* q_win, const void* keys, int32_t slots, int32_t group,
+                            int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,
+                            int64_t q_base, double p, double scale, const float* stat_max, const float* stat_sum,
+                            int64_t stat_ld, int64_t stat_row0, float* row_max, float* row_sum, float* col_partial,
+                            uint64_t* below_head, int32_t* below_col, void* exact_ws, int64_t exact_ws_bytes,
+                            void* stream) {
     if (!q_win || !keys || !row_max || !row_sum || !col_partial || !below_head)
         return fail(VLC_EINVAL, "score_stats: null pointer");
     if (slots < 1 || group < 1 || window < 1 || n_keys < 1 || q_base < 0)
@@ -103,6 +134,7 @@ int vlc_score_stats(const void* q_win, const void* keys, int32_t slots, int32_t 
     a.below_head = reinterpret_cast<unsigned long long*>(below_head);
     a.below_col = below_col;
     a.inv_scale_d = scale > 0.0 ? scale : 1.0 / std::sqrt((double)head_dim);
+    a.stat_max = stat_max; a.stat_sum = stat_sum; a.stat_ld = stat_ld; a.stat_row0 = stat_row0;
     if (exact_ws) {
         const int64_t rows = (int64_t)group * window;
         const int cap = vlc::exact_ws_cap(exact_ws_bytes, slots, rows);

@@ -50,6 +50,12 @@ struct ScoreArgs {
     float band;                        // log2 units, K1's listing band
     float err_max;                     // logit units: |fp32 row max - exact row max| bound
     double inv_scale_d;                // the reference's 1/sqrt(d) (or scale) in double
+    // row statistics given (f2 fusion): the prefill's exact row max (logit
+    // units) and row sum of every prompt row; K1 then runs pass 2 only.
+    // Row i of head g in slot s is at ((s*G + g) * stat_ld + stat_row0 + i).
+    const float* stat_max;
+    const float* stat_sum;
+    int64_t stat_ld, stat_row0;
 };
 int score_partials(int64_t rows);    // col_partial rows per slot for R window rows
 cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st);

@@ -224,6 +224,36 @@ class VLCache:
             if t.dim() != 5 or tuple(t.shape[:3]) != (s.B, s.L, s.Hkv) or t.shape[4] != s.d:
                 raise ValidationError(f"{name}: expected [B, L, Hkv, T, d], got {tuple(t.shape)}")
 
+    def score_stats_given(self, q_win, keys, stat_max, stat_sum):
+        """K1's column pass only, with the window rows' softmax statistics from the
+        prefill (stat_max logit units / stat_sum f32 [B, L, Hq, m]): row f2's fusion."""
+        s = self.shape
+        self._check_inputs(q_win, keys)
+        if tuple(stat_max.shape[-1:]) != (s.m,) or stat_max.numel() != s.B * s.L * s.Hq * s.m:
+            raise ValidationError(f"stat_max: expected [B, L, Hq, {s.m}] prefill statistics")
+        _lib.call("vlc_score_stats_given", q_win.data_ptr(), keys.data_ptr(), s.slots, s.G, s.d,
+                  keys.shape[3], s.m, s.w, s.m - s.w, self.p, self.scale, stat_max.data_ptr(), stat_sum.data_ptr(),
+                  s.m, _ptr(self.row_max), _ptr(self.row_sum), _ptr(self.col_partial), _ptr(self.below_head), 0,
+                  _ptr(self.exact_ws), self.exact_ws_bytes, _stream())
+
+    def prefill_compress(self, q_prompt, keys, values):
+        """Row f2 end to end: causal prefill of the m prompt rows (vlc_prefill,
+        returns its f32 [B, L, Hq, m, d] output), K1's column pass on the
+        prefill's own row statistics for the window rows, then K2 -> K3 -> K4.
+        q_prompt: bf16 [B, L, Hq, >= m, d]; keys / values as for compress()."""
+        from .prefill import prefill
+
+        s = self.shape
+        if self.head_shard is not None:
+            raise ValidationError("prefill_compress: head-sharded engines are not supported")
+        out, rmax, rsum = prefill(q_prompt, keys, values, s.m, scale=self.scale or None)
+        q_win = q_prompt[:, :, :, s.m - s.w:s.m].contiguous()
+        self.score_stats_given(q_win, keys, rmax, rsum)
+        self.allocate()
+        self.select()
+        self.gather(keys, values)
+        return out
+
     def compress(self, q_win, keys, values=None, group=None):
         """K1 -> (count exchange across ranks when head-sharded) -> K2 -> K3 -> K4."""
         self.score_stats(q_win, keys)

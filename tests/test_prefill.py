@@ -83,3 +83,35 @@ def test_gpu_prefill_validation():
     q = torch.zeros((1, 1, 2, 16, 64), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValidationError, match="m: must be"):
         prefill(q, q, q, 17)
+
+
+@pytest.mark.gpu
+def test_gpu_prefill_compress_equals_compress():
+    """Row f2's fusion: K1's column pass on the prefill's own row statistics gives
+    the same below counts, budgets and kept sets as the two-pass K1 (generator
+    inputs, 4 layers of the M7B shapes; exact mode)."""
+    import torch
+
+    import bench
+    from paper_2410_23317_b200.engine import Shape, VLCache
+
+    c = bench.CFG
+    L, m, w = 4, c["prompt_len"], c["tau"]
+    qw, qd, ks, vs = bench.synth_inputs(1, 0, m, layers=L)
+    dev = lambda a: torch.from_numpy(a).to(torch.bfloat16).cuda()  # noqa: E731
+    q_all, keys, values = dev(qw), dev(ks), dev(vs)
+    shape = Shape(1, L, c["q_heads"], c["kv_heads"], c["head_dim"], m, w)
+    a = VLCache(shape, alpha=c["alpha"], decode_steps=4)
+    a.compress(q_all[:, :, :, m - w:m].contiguous(), keys, values)
+    b = VLCache(shape, alpha=c["alpha"], decode_steps=4)
+    out = b.prefill_compress(q_all, keys, values)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    assert torch.equal(a.below_head, b.below_head)
+    assert torch.equal(a.kept_counts, b.kept_counts)
+    torch.testing.assert_close(b.row_sum, a.row_sum, rtol=2e-6, atol=0)
+    assert torch.equal(a.row_max, b.row_max)
+    ka, kb = a.kept_sets(), b.kept_sets()
+    diff = sum(int((x != y).sum()) if x.shape == y.shape else 10**6
+               for la, lb in zip(ka[0], kb[0]) for x, y in zip(la, lb))
+    assert diff == 0

@@ -37,6 +37,35 @@ line = {"prefill_ms": ms, "attention_tflops": flops / ms / 1e9, "flops": flops,
         "issued_tflops": 1.5 * flops / ms / 1e9, "note": "two-pass: 3 MMAs per tile (QK^T twice)"}
 if tc:
     line["frac_of_bf16_peak"] = flops / ms / 1e9 / tc
+# row f2's fusion at the bench workload (generator inputs): prefill + K1 column pass
+# on the prefill's statistics + K2-K4, vs prefill followed by the two-pass compress
+import bench  # noqa: E402
+from paper_2410_23317_b200.engine import Shape, VLCache  # noqa: E402
+
+c = bench.CFG
+qa, _, ka, va = bench.synth_inputs(1, 0, M)
+dev = lambda x: torch.from_numpy(x).to(torch.bfloat16).cuda()  # noqa: E731
+qa, ka, va = dev(qa), dev(ka), dev(va)
+shape = Shape(1, L, HQ, HKV, D, M, c["tau"])
+eng = VLCache(shape, alpha=c["alpha"], decode_steps=c["n_out"] - 1)
+qwin = qa[:, :, :, M - c["tau"]:].contiguous()
+
+
+def timed(fn, reps=6):
+    out = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        out.append(a.elapsed_time(b))
+    return float(np.median(out[1:]))
+
+
+line["fused_prefill_compress_ms"] = timed(lambda: eng.prefill_compress(qa, ka, va))
+line["prefill_then_compress_ms"] = timed(lambda: (prefill(qa, ka, va, M, stats=False), eng.compress(qwin, ka, va)))
 # CPU: the reference algorithm (float32 numpy, tile 128) on one layer
 if os.environ.get("CPU", "1") == "1":
     from oracle import oracle as O
