@@ -37,7 +37,7 @@ struct PL {
     static constexpr uint32_t kK = KB * kN * 128;        // one K tile
     static constexpr uint32_t kV = 2 * D * 128;          // one V^T tile: D rows x 128 keys
     static constexpr uint32_t kP = 2 * kM * 128;         // P: 128 rows x 128 keys
-    static constexpr uint32_t kBytes = kQ + 2 * kK + 2 * kV + kP + 1024;
+    static constexpr uint32_t kBytes = kQ + 2 * kK + 2 * kV + 2 * kP + 1024;   // 225 KB at d = 128
 };
 
 VLC_DEV uint32_t pack_bf16(float lo, float hi) {
@@ -63,10 +63,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     uint8_t* sk = sq + LY::kQ;
     uint8_t* sv = sk + 2 * LY::kK;
     uint8_t* sp = sv + 2 * LY::kV;
-    __shared__ uint64_t qfull, kfull[2], kempty[2], vfull[2], vempty[2], tfull[2], tempty[2], pfull, pempty, ofull;
+    __shared__ uint64_t qfull, kfull[2], kempty[2], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
+        ofull;
     __shared__ uint32_t tmem_slot;
-    __shared__ float2 rowstat[4 * kM];
     __shared__ float c_mb[kM], c_il[kM];
+    float2* rowstat = reinterpret_cast<float2*>(sp);   // [4 * kM], pass 1 only (P is pass 2 only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sq_slot = blockIdx.y;                                  // (b, l, query head)
@@ -83,8 +84,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1);
             sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kEpiWarps);
         }
-        sm100::mbar_init(&pfull, kEpiWarps);
-        sm100::mbar_init(&pempty, 1);
+        for (int i = 0; i < 2; ++i) { sm100::mbar_init(pfull + i, kEpiWarps); sm100::mbar_init(pempty + i, 1); }
         sm100::mbar_init(&ofull, 1);
         sm100::fence_barrier_init();
     }
@@ -144,9 +144,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 sm100::mma_commit(kempty + st);
                 sm100::mma_commit(tfull + st);
             };
-            auto pv = [&](int t) {    // O += P V for key tile t
+            auto pv = [&](int t) {    // O += P V for key tile t (P buffer and V^T stage t & 1)
                 const int st = t & 1;
-                sm100::mbar_wait(&pfull, t & 1);
+                sm100::mbar_wait(pfull + st, (t >> 1) & 1);
                 sm100::mbar_wait(vfull + st, (t >> 1) & 1);
                 sm100::tc_fence_after();
                 const uint32_t v_addr = sm100::smem_u32(sv + st * LY::kV);
@@ -154,10 +154,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        sm100::mma_bf16(tmem_o, sm100::sdesc_k_sw128(p_addr + kb * kM * 128 + kk * 32),
+                        sm100::mma_bf16(tmem_o, sm100::sdesc_k_sw128(p_addr + st * LY::kP + kb * kM * 128 + kk * 32),
                                         sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32), idesc_o,
                                         (t | kb | kk) != 0);
-                sm100::mma_commit(&pempty);
+                sm100::mma_commit(pempty + st);
                 sm100::mma_commit(vempty + st);
             };
             sm100::mbar_wait(&qfull, 0);
@@ -192,17 +192,28 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + st);
             const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
+            const bool full = __all_sync(kFull, valid == 32);
             float cmax = -INFINITY;
+            if (full) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+                for (int k = 0; k < 32; ++k) cmax = fmaxf(cmax, l[k]);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+            }
             if (cmax > m) {
                 sum *= ex2((m - cmax) * c1);
                 m = cmax;
             }
             const float mb = m * c1;
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            if (full) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) acc[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                for (int k = 0; k < 32; ++k) acc[k & 3] += ex2(fmaf(l[k], c1, -mb));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) acc[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+            }
             sum += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
         rowstat[cg * kM + li] = make_float2(m, sum);
@@ -238,20 +249,28 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             if (lane == 0) sm100::mbar_arrive(tempty + st);
             const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
             uint32_t pk[16];
+            if (__all_sync(kFull, valid == 32)) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) * il : 0.f;
-                const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) * il : 0.f;
-                pk[k] = pack_bf16(p0, p1);
+                for (int k = 0; k < 16; ++k)
+                    pk[k] = pack_bf16(ex2(fmaf(l[2 * k], c1, -mb)) * il, ex2(fmaf(l[2 * k + 1], c1, -mb)) * il);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) * il : 0.f;
+                    const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) * il : 0.f;
+                    pk[k] = pack_bf16(p0, p1);
+                }
             }
-            sm100::mbar_wait(&pempty, (t & 1) ^ 1);                   // the previous P V has read P
+            const int pb = t & 1;
+            sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);       // P V of tile t - 2 has read this buffer
+            uint8_t* pdst = sp + pb * LY::kP;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(sp + swz(kM, li, cg * 4 + q)) =
+                *reinterpret_cast<uint4*>(pdst + swz(kM, li, cg * 4 + q)) =
                     make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
             sm100::fence_proxy_async();                              // generic writes -> async proxy
             __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(&pfull);
+            if (lane == 0) sm100::mbar_arrive(pfull + pb);
         }
 
         // O: thread = row, warp cg holds dims 32 cg .. 32 cg + 31
