@@ -343,7 +343,7 @@ class VLCache:
                   _ptr(self.col_partial) + slot0 * s.nrb * s.m * 4, _ptr(self.below_head) + slot0 * s.G * 8,
                   0, _ptr(self.exact_ws), self.exact_ws_bytes, _stream())
 
-    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4):
+    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4, dec_chunks=8, dec_early=2):
         """End-to-end call with pinned HOST inputs (the reference API's setting:
         traces live in host memory): copies Q windows, prompt keys, decode
         queries and the decode steps' K/V rows to the device, compresses --
@@ -386,27 +386,38 @@ class VLCache:
                     ev = torch.cuda.Event()
                     ev.record(cs)
                     groups.append((b, l0, l1, ev))
-            # decode inputs in step groups, so the first decode steps run while
-            # the later groups' rows are still crossing PCIe
-            n = q_dec.shape[3]
-            per_s = -(-n // max(1, int(chunks)))
-            steps = []
-            for s0 in range(0, n, per_s):
-                s1 = min(n, s0 + per_s)
-                for dst, src in ((d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
-                    rows = src.numel() // (n * s.d)           # B*L*H
-                    pitch = n * s.d * 2
-                    _lib.call("vlc_copy_2d", dst.data_ptr() + s0 * s.d * 2, pitch, src.data_ptr() + s0 * s.d * 2,
-                              pitch, (s1 - s0) * s.d * 2, rows, cs.cuda_stream)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-                steps.append((s0, s1, ev))
+        # decode inputs in step groups: the first `dec_early` groups cross PCIe
+        # right behind the keys (filling the link while K1's last group, K2 and
+        # K3 run); the rest are queued behind K4 so they do not compete with its
+        # zero-copy value reads, and the decode chases them group by group
+        n = q_dec.shape[3]
+        per_s = -(-n // max(1, int(dec_chunks)))
+        bounds = [(s0, min(n, s0 + per_s)) for s0 in range(0, n, per_s)]
+        steps = []
+
+        def copy_steps(part):
+            with torch.cuda.stream(cs):
+                for s0, s1 in part:
+                    for dst, src in ((d_qd, q_dec), (d_kn, k_dec), (d_vn, v_dec)):
+                        rows = src.numel() // (n * s.d)           # B*L*H
+                        pitch = n * s.d * 2
+                        _lib.call("vlc_copy_2d", dst.data_ptr() + s0 * s.d * 2, pitch,
+                                  src.data_ptr() + s0 * s.d * 2, pitch, (s1 - s0) * s.d * 2, rows, cs.cuda_stream)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    steps.append((s0, s1, ev))
+
+        copy_steps(bounds[:dec_early])
         for b, l0, l1, ev in groups:
             comp.wait_event(ev)
             self.score_stats_layers(d_qw, d_k, b, l0, l1)
         self.allocate()
         self.select()
         self.gather(d_k, v_prompt)             # keys from the device copy, values zero-copy
+        k4_done = torch.cuda.Event()
+        k4_done.record(comp)
+        cs.wait_event(k4_done)
+        copy_steps(bounds[dec_early:])
         for s0, s1, ev in steps:
             if s0 >= self.decode_steps:
                 break
