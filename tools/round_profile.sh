@@ -16,3 +16,10 @@ ncu --graph-profiling node --cache-control none --clock-control none -k regex:de
     --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
     python tools/k5_graph_run.py > $O/k5_traffic_$TAG.csv 2>&1
 ls -la $O
+# f2 prefill (4 layers of the M7B shapes) and the f2/f4 timing tools
+ncu --set full --import-source on --clock-control none -k regex:prefill_kernel -s 1 -c 1 \
+    -o $O/prefill_$TAG python tools/prefill_once.py > /dev/null 2>&1
+timeout 600 python tools/prefill_bench.py > $O/prefill_bench_$TAG.json 2> $O/prefill_bench_$TAG.err
+timeout 600 python tools/eval_bench.py 8 32 > $O/eval_bench_$TAG.txt 2>&1
+timeout 900 python tools/configs_bench.py --out $O/configs_$TAG.json > $O/configs_$TAG.log 2>&1
+ls -la $O
