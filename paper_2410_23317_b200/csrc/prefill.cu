@@ -8,9 +8,11 @@
 //
 // Two passes per CTA = (query head, block of 128 prompt rows), like K1:
 //   pass 1: S = Q K^T tile by tile (TMEM) -> exact row max / sum (thread = row)
-//   pass 2: S again -> P = 2^(S c1 - max c1) / sum as bf16 into shared memory
-//           (the UMMA A layout, 128-byte swizzle) -> O += P V^T^T on tcgen05
-//           with V^T tiles (pre-transposed once, K-major) as the B operand.
+//   pass 2: S again -> P = 2^(S c1 - max c1) / sum as bf16 into tensor memory
+//           (tcgen05.st; two P stages of 64 packed columns) -> O += P V on
+//           tcgen05 with A = P read from TMEM and B = V^T tiles (pre-transposed
+//           once, K-major) from shared memory.  VLC_PF_TS=0 builds the variant
+//           that stages P in shared memory (UMMA A layout, 128-byte swizzle).
 // The row max is final before any P is formed, so O accumulates in TMEM with
 // no rescaling; the cost is one extra Q K^T (3 MMAs per tile instead of 2).
 // Warps: 0 K producer, 1 MMA issuer, 2 TMEM allocator, 3 V^T producer,
@@ -28,7 +30,12 @@ constexpr int kM = 128;          // rows per CTA
 constexpr int kN = 128;          // keys per tile
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr uint32_t kTmemCols = 512;   // S: 2 x 128, O: d <= 128
+constexpr uint32_t kTmemCols = 512;   // S: 2 x 128, O: d <= 128, P (TS mode): 2 x 64
+#ifndef VLC_PF_TS
+#define VLC_PF_TS 1
+#endif
+constexpr bool kTS = VLC_PF_TS;       // P through TMEM (A operand from tensor memory) instead of smem
+constexpr int kKS = 2;                 // K tile ring (a third stage measured no faster)
 
 template <int D>
 struct PL {
@@ -37,7 +44,8 @@ struct PL {
     static constexpr uint32_t kK = KB * kN * 128;        // one K tile
     static constexpr uint32_t kV = 2 * D * 128;          // one V^T tile: D rows x 128 keys
     static constexpr uint32_t kP = 2 * kM * 128;         // P: 128 rows x 128 keys
-    static constexpr uint32_t kBytes = kQ + 2 * kK + 2 * kV + 2 * kP + 1024;   // 225 KB at d = 128
+    static constexpr uint32_t kPArea = kTS ? 4 * kM * 8 : 2 * kP;     // TS: pass 1's row statistics only
+    static constexpr uint32_t kBytes = kQ + kKS * kK + 2 * kV + kPArea + 1024;
 };
 
 VLC_DEV uint32_t pack_bf16(float lo, float hi) {
@@ -48,7 +56,7 @@ VLC_DEV uint32_t pack_bf16(float lo, float hi) {
 
 // byte offset of 16-byte chunk c (8 bf16) of row r in a 128B-swizzled tile of
 // `rows` rows (64-element boxes, `rows` x 128 B each) -- the TMA / UMMA layout
-VLC_DEV uint32_t swz(int rows, int r, int c) {
+[[maybe_unused]] VLC_DEV uint32_t swz(int rows, int r, int c) {
     return (uint32_t)((c >> 3) * rows * 128 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
@@ -61,9 +69,9 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sq = smem;
     uint8_t* sk = sq + LY::kQ;
-    uint8_t* sv = sk + 2 * LY::kK;
+    uint8_t* sv = sk + kKS * LY::kK;
     uint8_t* sp = sv + 2 * LY::kV;
-    __shared__ uint64_t qfull, kfull[2], kempty[2], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
+    __shared__ uint64_t qfull, kfull[kKS], kempty[kKS], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
         ofull;
     __shared__ uint32_t tmem_slot;
     __shared__ float c_mb[kM], c_il[kM];
@@ -79,8 +87,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 
     if (threadIdx.x == 0) {
         sm100::mbar_init(&qfull, 1);
+        for (int i = 0; i < kKS; ++i) { sm100::mbar_init(kfull + i, 1); sm100::mbar_init(kempty + i, 1); }
         for (int i = 0; i < 2; ++i) {
-            sm100::mbar_init(kfull + i, 1); sm100::mbar_init(kempty + i, 1);
             sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1);
             sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kEpiWarps);
         }
@@ -94,6 +102,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     sm100::tc_fence_after();
     const uint32_t tmem = tmem_slot;
     const uint32_t tmem_o = tmem + 2 * kN;
+    const uint32_t tmem_p = tmem + 3 * kN;                            // TS mode: P stages, 64 columns each
 
     if (warp < 4) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n");
@@ -105,8 +114,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             for (int kb = 0; kb < LY::KB; ++kb)
                 sm100::tma_load_2d(sq + kb * kM * 128, &qmap, &qfull, kb * 64, (int)(sq_slot * a.q_rows + r0));
             for (int it = 0; it < 2 * T; ++it) {
-                const int st = it & 1, t = it < T ? it : it - T;
-                sm100::mbar_wait(kempty + st, ((it >> 1) & 1) ^ 1);
+                const int st = it % kKS, t = it < T ? it : it - T;
+                sm100::mbar_wait(kempty + st, ((it / kKS) & 1) ^ 1);
                 sm100::mbar_expect_tx(kfull + st, LY::kK);
                 for (int kb = 0; kb < LY::KB; ++kb)
                     sm100::tma_load_2d(sk + st * LY::kK + kb * kN * 128, &kmap, kfull + st, kb * 64,
@@ -129,11 +138,11 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             constexpr uint32_t idesc_o = sm100::idesc_bf16_f32(kM, D);
             const uint32_t q_addr = sm100::smem_u32(sq), p_addr = sm100::smem_u32(sp);
             auto qk = [&](int it) {   // S[it & 1] = Q K^T of the K tile in ring stage it & 1
-                const int st = it & 1;
+                const int st = it & 1, ks = it % kKS;
                 sm100::mbar_wait(tempty + st, ((it >> 1) & 1) ^ 1);
-                sm100::mbar_wait(kfull + st, (it >> 1) & 1);
+                sm100::mbar_wait(kfull + ks, (it / kKS) & 1);
                 sm100::tc_fence_after();
-                const uint32_t k_addr = sm100::smem_u32(sk + st * LY::kK);
+                const uint32_t k_addr = sm100::smem_u32(sk + ks * LY::kK);
 #pragma unroll
                 for (int kb = 0; kb < LY::KB; ++kb)
 #pragma unroll
@@ -141,7 +150,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                         sm100::mma_bf16(tmem + st * kN, sm100::sdesc_k_sw128(q_addr + kb * kM * 128 + kk * 32),
                                         sm100::sdesc_k_sw128(k_addr + kb * kN * 128 + kk * 32), idesc_s,
                                         (kb | kk) != 0);
-                sm100::mma_commit(kempty + st);
+                sm100::mma_commit(kempty + ks);
                 sm100::mma_commit(tfull + st);
             };
             auto pv = [&](int t) {    // O += P V for key tile t (P buffer and V^T stage t & 1)
@@ -153,10 +162,15 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                 for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk)
-                        sm100::mma_bf16(tmem_o, sm100::sdesc_k_sw128(p_addr + st * LY::kP + kb * kM * 128 + kk * 32),
-                                        sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32), idesc_o,
-                                        (t | kb | kk) != 0);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const uint64_t bd = sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32);
+                        if constexpr (kTS)   // 16 keys = 8 packed columns per instruction
+                            sm100::mma_bf16_ts(tmem_o, tmem_p + st * 64 + (kb * 4 + kk) * 8, bd, idesc_o,
+                                               (t | kb | kk) != 0);
+                        else
+                            sm100::mma_bf16(tmem_o, sm100::sdesc_k_sw128(p_addr + st * LY::kP + kb * kM * 128 + kk * 32),
+                                            bd, idesc_o, (t | kb | kk) != 0);
+                    }
                 sm100::mma_commit(pempty + st);
                 sm100::mma_commit(vempty + st);
             };
@@ -263,12 +277,19 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             }
             const int pb = t & 1;
             sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);       // P V of tile t - 2 has read this buffer
-            uint8_t* pdst = sp + pb * LY::kP;
+            if constexpr (kTS) {
+                // this warp's 32 keys = 16 packed columns of its lane quarter
+                sm100::tc_fence_after();
+                sm100::tmem_st16(tmem_p + (uint32_t(32 * sub) << 16) + pb * 64 + cg * 16, pk);
+                sm100::tc_fence_before();
+            } else {
+                uint8_t* pdst = sp + pb * LY::kP;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                *reinterpret_cast<uint4*>(pdst + swz(kM, li, cg * 4 + q)) =
-                    make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            sm100::fence_proxy_async();                              // generic writes -> async proxy
+                for (int q = 0; q < 4; ++q)
+                    *reinterpret_cast<uint4*>(pdst + swz(kM, li, cg * 4 + q)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                sm100::fence_proxy_async();                          // generic writes -> async proxy
+            }
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(pfull + pb);
         }
