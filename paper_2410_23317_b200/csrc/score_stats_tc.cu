@@ -41,15 +41,24 @@ constexpr int kN = 128;          // keys per tile (UMMA N)
 #endif
 constexpr int kStages = VLC_K1_STAGES;   // K tile ring
 constexpr int kSub = VLC_K1_SUB;         // TMEM columns an epilogue thread holds at a time (16 / 32)
-constexpr int kEpiWarps = 16;    // two sets of 8, one per accumulator stage
-constexpr int kSetWarps = kEpiWarps / 2;   // 4 lane quarters x 2 column halves of 64
+#ifndef VLC_K1_SETS
+#define VLC_K1_SETS 2
+#endif
+constexpr int kSets = VLC_K1_SETS;          // epilogue warp sets taking tiles round robin
+constexpr int kSetWarps = 8;                // 4 lane quarters x 2 column halves of 64
+constexpr int kEpiWarps = kSets * kSetWarps;
 constexpr int kCh = 64 / kSub;             // TMEM loads per warp and tile
 constexpr int kThreads = 128 + kEpiWarps * 32;
 #ifndef VLC_K1_ACC
-#define VLC_K1_ACC 4
+#define VLC_K1_ACC (kSets == 2 ? 4 : kSets)
 #endif
-constexpr int kAcc = VLC_K1_ACC;           // accumulator stages (2 or 4; set p owns stages = p mod 2)
-constexpr uint32_t kTmemCols = kAcc * kN;
+constexpr int kAcc = VLC_K1_ACC;           // accumulator stages (a multiple of kSets; set p owns stages = p mod kSets)
+static_assert(kAcc % kSets == 0 && kAcc * 128 <= 512, "accumulator stages");
+// registers: launch at 65536 / threads, then the control warpgroup drops to 32
+// and the epilogue warpgroups take the rest (setmaxnreg)
+constexpr int kRegLaunch = (65536 / (128 + kEpiWarps * 32)) & ~7;
+constexpr int kRegEpi = ((kRegLaunch * (128 + kEpiWarps * 32) - 128 * 32) / (kEpiWarps * 32)) & ~7;
+constexpr uint32_t kTmemCols = kAcc * kN <= 256 ? 256u : 512u;   // tcgen05.alloc: a power of two
 
 template <int D>
 struct Layout {
@@ -89,7 +98,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     // small state in static shared memory (plain LDS/STS, not generic accesses)
     __shared__ uint64_t full[kStages], empty[kStages], qfull[1], tfull[kAcc], tempty[kAcc];
     __shared__ uint32_t tmem_slot[1];
-    __shared__ float2 rowstat[4 * kM];                  // (max, sum) per (set, column half) and row
+    __shared__ float2 rowstat[2 * kSets * kM];          // (max, sum) per (set, column half) and row
     __shared__ __align__(16) float c_mb[kM];            // row max (raw dot) * c1
     __shared__ __align__(16) float c_is[kM];            // 1 / row sum (0: no row)
     __shared__ __align__(16) float c_t2[kM];            // threshold on u (-inf: no row)
@@ -176,13 +185,13 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             }
         }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegEpi));
         // ------------------------------------------------ epilogue
         // Two warp sets, set p taking tiles it = p (mod 2) from accumulator stages
         // p and p + 2, so one set's TMEM-load latency overlaps the other's math and
         // the MMA runs a tile ahead of each set.  Within a set,
         // warp -> (TMEM lane quarter `sub`, 64-column half `half`).
-        const int ew = warp - 4, sub = warp & 3, set = ew >> 3, half = (ew >> 2) & 1;
+        const int ew = warp - 4, sub = warp & 3, set = ew >> 3, half = (ew >> 2) & 1;   // 8 warps per set
         const int lane_idx = 32 * sub + lane;                  // TMEM lane of this thread
         const uint32_t lane_addr = tmem + (uint32_t(32 * sub) << 16) + half * 64;
         const float c1 = a.inv_scale * kLog2e;
@@ -195,7 +204,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int64_t i = row_ok ? r % a.w : 0;
             const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
             float m = -INFINITY, sum = 0.f;
-            for (int it = set; it < P1; it += 2) {
+            for (int it = set; it < P1; it += kSets) {
                 const int acc = it % kAcc;
                 sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
                 sm100::tc_fence_after();
@@ -244,9 +253,9 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     mb = rm * kLog2e;
                 } else {
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
+                    for (int g4 = 0; g4 < 2 * kSets; ++g4) M = fmaxf(M, rowstat[g4 * kM + lane_idx].x);
 #pragma unroll
-                    for (int g4 = 0; g4 < 4; ++g4) {
+                    for (int g4 = 0; g4 < 2 * kSets; ++g4) {
                         const float2 h = rowstat[g4 * kM + lane_idx];
                         if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
                     }
@@ -279,7 +288,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const int64_t rg = r_first + r0;
         const bool one_head = rg / a.w == (rg + 63) / a.w;
         float* colp = a.col_partial + ((int64_t)s * nparts + rb * 2 + half) * a.n;
-        for (int it = P1 + ((P1 ^ set) & 1); it < iters; it += 2) {
+        for (int it = P1 + (set - P1 % kSets + kSets) % kSets; it < iters; it += kSets) {
             const int t = it - P1;
             const int j = t * kN + lane_idx;                     // this thread's key
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform

@@ -1,3 +1,5 @@
-for v in default exp_libs/acc2.so; do
-  if [ $v = default ]; then python tools/k1_exact_cost.py 2>&1 | grep "K1\|score_stats_tc"; else VLC_LIB_PATH=$v python tools/k1_exact_cost.py 2>&1 | grep "K1\|score_stats_tc"; fi
+# K1 timing (generator inputs, exact on/off) for the in-tree library and exp_libs/*.so variants
+for v in default "$@"; do
+  echo "== $v"
+  if [ "$v" = default ]; then python tools/k1_exact_cost.py 2>&1 | grep "generator"; else VLC_LIB_PATH=$v python tools/k1_exact_cost.py 2>&1 | grep "generator"; fi
 done
