@@ -115,3 +115,34 @@ def test_gpu_prefill_compress_equals_compress():
     diff = sum(int((x != y).sum()) if x.shape == y.shape else 10**6
                for la, lb in zip(ka[0], kb[0]) for x, y in zip(la, lb))
     assert diff == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("B,L,HQ,HKV,D,M,W", [(2, 2, 8, 2, 64, 700, 64), (1, 2, 4, 4, 128, 333, 32)])
+def test_gpu_prefill_compress_random_inputs(B, L, HQ, HKV, D, M, W):
+    """Fusion on dense near-threshold mass (random logits; exact mode re-decides
+    many entries): identical counts and budgets; kept sets equal up to score
+    near-ties at the boundary (the mass uses max*log2e instead of raw max * c1)."""
+    import torch
+
+    from paper_2410_23317_b200.engine import Shape, VLCache
+    from test_gpu_parity import check_kept_sets
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q = (torch.randn((B, L, HQ, M + 5, D), device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    k = torch.randn((B, L, HKV, M + 5, D), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((B, L, HKV, M + 5, D), device="cuda", generator=g).to(torch.bfloat16)
+    shape = Shape(B, L, HQ, HKV, D, M, W)
+    a = VLCache(shape, alpha=0.2, decode_steps=2, keep_scores=True)
+    a.compress(q[:, :, :, M - W:M].contiguous(), k, v)
+    b = VLCache(shape, alpha=0.2, decode_steps=2)
+    out = b.prefill_compress(q, k, v)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    assert torch.equal(a.below_head, b.below_head)
+    assert torch.equal(a.kept_counts, b.kept_counts)
+    counts = a.kept_counts.view(B, L).cpu().numpy()
+    scores = a.scores.view(B, L, HKV, M).cpu().numpy()
+    ka, kb = a.kept_sets(), b.kept_sets()
+    for bb in range(B):
+        check_kept_sets(kb[bb], ka[bb], scores[bb], counts[bb])
