@@ -26,7 +26,7 @@ from dataclasses import dataclass
 from . import _lib
 from .errors import DegenerateSparsityError, ValidationError
 
-_ROW_BLOCK = 128  # K1 rows per CTA; col_partial has 4 partials (32-row groups) per block
+_ROW_BLOCK = 128  # K1 rows per CTA; col_partial has 2 partials (64-row halves) per block
 
 
 def _ptr(t) -> int:

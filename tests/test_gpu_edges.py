@@ -1,6 +1,6 @@
 """Edge cases of the sm_100a path against the CPU oracle (bf16-in protocol).
 
-Windows that straddle 32-row groups and heads, single-row windows, prefill-
+Windows that straddle 64-row halves and heads, single-row windows, prefill-
 sized windows (many 128-row blocks), extreme budgets and reserve fractions,
 very long score rows (the global-scratch radix select) and empty/size-one
 decode caches -- the shapes the reference's own tests exercise
@@ -21,7 +21,7 @@ from test_gpu_parity import bf16, check_kept_sets, make_inputs  # noqa: E402
 
 
 @pytest.mark.parametrize("layers,hq,hkv,d,m,tau,alpha,recent", [
-    (2, 8, 2, 64, 300, 12, 0.1, 0.1),      # 48-row slots: heads straddle 32-row groups
+    (2, 8, 2, 64, 300, 12, 0.1, 0.1),      # 48-row slots: heads straddle 64-row halves
     (2, 8, 8, 64, 200, 1, 0.1, 0.1),       # single-row windows
     (1, 4, 2, 64, 260, 260, 0.1, 0.1),     # prefill window: 520 rows, 5 row blocks
     (3, 4, 4, 128, 400, 40, 1.0, 0.1),     # alpha = 1 (clipped budgets)
