@@ -7,14 +7,16 @@
 // prefill's Q K^T).
 //
 // Two passes per CTA = (query head, block of 128 prompt rows), like K1:
-//   pass 1: S = Q K^T tile by tile (TMEM) -> exact row max / sum (thread = row)
-//   pass 2: S again -> P = 2^(S c1 - max c1) / sum as bf16 into tensor memory
+//   pass 1: S = Q K^T tile by tile (TMEM) -> exact row max (thread = row; no exp)
+//   pass 2: S again -> P = 2^(S c1 - max c1) <= 1 as bf16 into tensor memory
 //           (tcgen05.st; two P stages of 64 packed columns) -> O += P V on
 //           tcgen05 with A = P read from TMEM and B = V^T tiles (pre-transposed
 //           once, K-major) from shared memory.  VLC_PF_TS=0 builds the variant
 //           that stages P in shared memory (UMMA A layout, 128-byte swizzle).
 // The row max is final before any P is formed, so O accumulates in TMEM with
-// no rescaling; the cost is one extra Q K^T (3 MMAs per tile instead of 2).
+// no rescaling and is divided by the row sum (accumulated alongside P) once at
+// the end; one exponential per entry; the cost is one extra Q K^T (3 MMAs per
+// tile instead of 2) and a max-only first pass.
 // Warps: 0 K producer, 1 MMA issuer, 2 TMEM allocator, 3 V^T producer,
 // 4-19 epilogue (lane quarter x 32-column group).
 #include <cuda.h>
@@ -74,7 +76,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ uint64_t qfull, kfull[kKS], kempty[kKS], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
         ofull;
     __shared__ uint32_t tmem_slot;
-    __shared__ float c_mb[kM], c_il[kM];
+    __shared__ float c_mb[kM], c_part[4 * kM];
     float2* rowstat = reinterpret_cast<float2*>(sp);   // [4 * kM], pass 1 only (P is pass 2 only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -195,8 +197,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const float c1 = a.inv_scale * kLog2e;
         float l[32];
 
-        // pass 1: running max of the raw dots and rescaled sum of 2^(.)
-        float m = -INFINITY, sum = 0.f;
+        // pass 1: row max of the raw dots only (no exponentials)
+        float m = -INFINITY;
         for (int it = 0; it < T; ++it) {
             const int st = it & 1;
             sm100::mbar_wait(tfull + st, (it >> 1) & 1);
@@ -206,53 +208,29 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(tempty + st);
             const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
-            const bool full = __all_sync(kFull, valid == 32);
-            float cmax = -INFINITY;
-            if (full) {
+            if (__all_sync(kFull, valid == 32)) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) cmax = fmaxf(cmax, l[k]);
+                for (int k = 0; k < 32; ++k) m = fmaxf(m, l[k]);
             } else {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) cmax = k < valid ? fmaxf(cmax, l[k]) : cmax;
+                for (int k = 0; k < 32; ++k) m = k < valid ? fmaxf(m, l[k]) : m;
             }
-            if (cmax > m) {
-                sum *= ex2((m - cmax) * c1);
-                m = cmax;
-            }
-            const float mb = m * c1;
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            if (full) {
-#pragma unroll
-                for (int k = 0; k < 32; ++k) acc[k & 3] += ex2(fmaf(l[k], c1, -mb));
-            } else {
-#pragma unroll
-                for (int k = 0; k < 32; ++k) acc[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
-            }
-            sum += (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
-        rowstat[cg * kM + li] = make_float2(m, sum);
+        rowstat[cg * kM + li] = make_float2(m, 0.f);
         sm100::named_bar_sync(1, kEpiWarps * 32);
         if (cg == 0) {
-            float M = -INFINITY, S = 0.f;
+            float M = -INFINITY;
 #pragma unroll
             for (int g = 0; g < 4; ++g) M = fmaxf(M, rowstat[g * kM + li].x);
-#pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                const float2 h = rowstat[g * kM + li];
-                if (h.x != -INFINITY) S += h.y * ex2((h.x - M) * c1);
-            }
             c_mb[li] = row_ok ? M * c1 : 0.f;
-            c_il[li] = row_ok ? 1.f / S : 0.f;
-            if (row_ok && a.row_max) {
-                a.row_max[(int64_t)sq_slot * a.m + r] = M * a.inv_scale;
-                a.row_sum[(int64_t)sq_slot * a.m + r] = S;
-            }
+            if (row_ok && a.row_max) a.row_max[(int64_t)sq_slot * a.m + r] = M * a.inv_scale;
         }
         sm100::named_bar_sync(1, kEpiWarps * 32);
-        const float mb = c_mb[li], il = c_il[li];
+        const float mb = c_mb[li];
 
-        // pass 2: P = 2^(l c1 - mb) / S (0 past the causal frontier) as bf16 into
-        // the A-operand layout, then the MMA warp adds P V into O
+        // pass 2: P = 2^(l c1 - mb) <= 1 (0 past the causal frontier) as bf16,
+        // the row sum of the same exponentials on the side; O = (P V) / sum at the end
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
         for (int t = 0; t < T; ++t) {
             const int it = T + t, st = it & 1;
             sm100::mbar_wait(tfull + st, (it >> 1) & 1);
@@ -265,13 +243,19 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             uint32_t pk[16];
             if (__all_sync(kFull, valid == 32)) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    pk[k] = pack_bf16(ex2(fmaf(l[2 * k], c1, -mb)) * il, ex2(fmaf(l[2 * k + 1], c1, -mb)) * il);
+                for (int k = 0; k < 16; ++k) {
+                    const float p0 = ex2(fmaf(l[2 * k], c1, -mb)), p1 = ex2(fmaf(l[2 * k + 1], c1, -mb));
+                    ps[(2 * k) & 3] += p0;
+                    ps[(2 * k + 1) & 3] += p1;
+                    pk[k] = pack_bf16(p0, p1);
+                }
             } else {
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
-                    const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) * il : 0.f;
-                    const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) * il : 0.f;
+                    const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) : 0.f;
+                    const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) : 0.f;
+                    ps[(2 * k) & 3] += p0;
+                    ps[(2 * k + 1) & 3] += p1;
                     pk[k] = pack_bf16(p0, p1);
                 }
             }
@@ -293,6 +277,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             __syncwarp();
             if (lane == 0) sm100::mbar_arrive(pfull + pb);
         }
+        // row sums: the four column groups' partials in a fixed order
+        c_part[cg * kM + li] = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        sm100::named_bar_sync(1, kEpiWarps * 32);
+        const float S = (c_part[li] + c_part[kM + li]) + (c_part[2 * kM + li] + c_part[3 * kM + li]);
+        if (cg == 0 && row_ok && a.row_sum) a.row_sum[(int64_t)sq_slot * a.m + r] = S;
+        const float il = row_ok ? 1.f / S : 0.f;
 
         // O: thread = row, warp cg holds dims 32 cg .. 32 cg + 31
         sm100::mbar_wait(&ofull, 0);
@@ -302,7 +292,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             if (row_ok) {
                 float4* dst = reinterpret_cast<float4*>(a.out + ((int64_t)sq_slot * a.m + r) * D + cg * 32);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) dst[q] = make_float4(l[4 * q], l[4 * q + 1], l[4 * q + 2], l[4 * q + 3]);
+                for (int q = 0; q < 8; ++q)
+                    dst[q] = make_float4(l[4 * q] * il, l[4 * q + 1] * il, l[4 * q + 2] * il, l[4 * q + 3] * il);
             }
         }
     }
