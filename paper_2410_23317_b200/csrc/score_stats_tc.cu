@@ -36,6 +36,9 @@ constexpr int kN = 128;          // keys per tile (UMMA N)
 #ifndef VLC_K1_SUB
 #define VLC_K1_SUB 32
 #endif
+#ifndef VLC_K1_SPLIT_TAIL
+#define VLC_K1_SPLIT_TAIL 1
+#endif
 #ifndef VLC_K1_MINB
 #define VLC_K1_MINB 1
 #endif
@@ -91,7 +94,7 @@ VLC_DEV void tmem_ld(uint32_t taddr, float (&v)[N]) {
 template <int D, bool EXACT>
 __global__ void __launch_bounds__(kThreads, VLC_K1_MINB)
 score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
-               ScoreArgs a, int nparts) {
+               ScoreArgs a, int nparts, int nblk, int n_full) {
     using LY = Layout<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -106,7 +109,14 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ int hcnt[kM];                            // below counts per head of the block
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s = blockIdx.y, rb = blockIdx.x;
+    // CTA -> (slot s, row block rb, key part).  The first n_full CTAs take whole
+    // units; the rest -- the units of the last, partial wave -- come in pairs
+    // that both run pass 1 (the row statistics need every key) and split pass
+    // 2's key tiles, so the tail wave takes about 0.7 of a unit instead of 1.
+    const int bid = blockIdx.x;
+    const int u = bid < n_full ? bid : n_full + (bid - n_full) / 2;
+    const int part = bid < n_full ? -1 : (bid - n_full) & 1;     // -1: whole unit
+    const int s = u / nblk, rb = u % nblk;
     const int64_t R = (int64_t)a.G * a.w;
     const int64_t r_first = (int64_t)rb * kM;
     const int64_t r_last = imin(R, r_first + kM) - 1;
@@ -114,7 +124,8 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     const int64_t blk_end = imin(a.n, a.q_base + i_max + 1);   // keys any row here can see
     const int T = (int)((blk_end + kN - 1) / kN);
     const int P1 = a.stat_max ? 0 : T;    // pass-1 tiles (none when the row statistics are given)
-    const int iters = P1 + T;
+    const int tlo = part == 1 ? (T + 1) / 2 : 0, thi = part == 0 ? (T + 1) / 2 : T;   // pass-2 key tiles
+    const int iters = P1 + (thi - tlo);
     const int64_t head0 = r_first / a.w;
 
     if (threadIdx.x == 0) {
@@ -145,7 +156,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             for (int it = 0; it < iters; ++it) {
                 const int st = it % kStages;
                 const uint32_t ph = (it / kStages) & 1;
-                const int t = it < P1 ? it : it - P1;
+                const int t = it < P1 ? it : tlo + (it - P1);
                 sm100::mbar_wait(empty + st, ph ^ 1);
                 sm100::mbar_expect_tx(full + st, LY::kKBytes);
                 uint8_t* kdst = smem + LY::kQBytes + st * LY::kKBytes;
@@ -289,7 +300,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const bool one_head = rg / a.w == (rg + 63) / a.w;
         float* colp = a.col_partial + ((int64_t)s * nparts + rb * 2 + half) * a.n;
         for (int it = P1 + (set - P1 % kSets + kSets) % kSets; it < iters; it += kSets) {
-            const int t = it - P1;
+            const int t = tlo + (it - P1);
             const int j = t * kN + lane_idx;                     // this thread's key
             const bool all_visible = (int64_t)t * kN + kN - 1 <= a.q_base;   // CTA-uniform
             const int acc = it % kAcc;
@@ -383,7 +394,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             }
         }
         // columns no row of this block can see
-        if (set == 0)
+        if (set == 0 && thi == T)
             for (int64_t jj = (int64_t)T * kN + lane_idx; jj < a.n; jj += kN) colp[jj] = 0.f;
         sm100::named_bar_sync(1, kEpiWarps * 32);
         const int nheads = (int)(r_last / a.w - head0 + 1);
@@ -408,8 +419,13 @@ cudaError_t launch_tc_e(const ScoreArgs& a, int nparts, cudaStream_t st) {
     const size_t sm = Layout<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(score_stats_tc<D, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    dim3 grid(nparts / 2, a.slots);
-    score_stats_tc<D, EXACT><<<grid, kThreads, sm, st>>>(qmap, kmap, a, nparts);
+    const int nblk = nparts / 2, units = nblk * a.slots;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int tail = units % n_sm;
+    const int n_full = (VLC_K1_SPLIT_TAIL && tail > 0 && 2 * tail <= n_sm) ? units - tail : units;
+    score_stats_tc<D, EXACT><<<n_full + 2 * (units - n_full), kThreads, sm, st>>>(qmap, kmap, a, nparts, nblk, n_full);
     return cudaGetLastError();
 }
 
