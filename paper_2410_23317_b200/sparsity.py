@@ -119,3 +119,43 @@ def decoding_sparsity(trace: AttentionTrace, config: SparsityConfig = SparsityCo
     if h.decode_len < 1:
         raise ValidationError("decode_len: trace has no decoding rows")
     return window_sparsity(trace, config, h.prompt_len, h.seq_len, phase="decoding")
+
+
+# ---------------------------------------------------------------- host analysis helpers
+# Small numpy utilities of the reference's analysis surface, kept on the host:
+# they act on per-layer curves (L values) or on caller-held arrays.
+
+def threshold_filter(a, p: float) -> np.ndarray:
+    """Copy of `a` (one row or rows) with entries below p * row max set to 0
+    (reference sparsity.py:46-66; the same filter K5-side contribution uses)."""
+    if not 0.0 < p < 1.0:
+        raise ValidationError(f"p: must be in (0, 1), got {p}")
+    x = np.asarray(a)
+    if x.size == 0:
+        raise ValidationError("input: must be non-empty")
+    if not np.isfinite(x).all():
+        raise ValidationError("input: must be finite")
+    if (x < 0).any():
+        raise ValidationError("input: must be non-negative")
+    if x.ndim > 2:
+        raise ValidationError(f"input: must be 1-D or 2-D, got {x.ndim}-D")
+    m2 = np.atleast_2d(x)
+    kept = np.where(m2 < p * m2.max(axis=1, keepdims=True), 0.0, m2)
+    return kept if x.ndim == 2 else kept[0]
+
+
+def curve_similarity(a: LayerSparsity, b: LayerSparsity) -> float:
+    """Pearson correlation of two per-layer head-mean sparsity curves
+    (reference sparsity.py:106-124); ZeroVarianceError for a flat curve."""
+    from .errors import ZeroVarianceError
+
+    x, y = a.layer_means(), b.layer_means()
+    if x.shape != y.shape:
+        raise ValidationError(f"curves: layer counts differ ({x.size} vs {y.size})")
+    if x.size < 2:
+        raise ValidationError("curves: need at least 2 layers")
+    dx, dy = x - x.mean(), y - y.mean()
+    sxx, syy = float(dx @ dx), float(dy @ dy)
+    if sxx == 0.0 or syy == 0.0:
+        raise ZeroVarianceError("curve variance is zero; correlation undefined")
+    return float(dx @ dy) / np.sqrt(sxx * syy)

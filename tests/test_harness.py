@@ -1,0 +1,95 @@
+"""The reference's benchmark harness (bench.py) on the B200: spec validation and
+memory accounting (CPU), and run_bench / the compression pass against golden
+outputs of the reference itself on bf16-rounded traces (GPU):
+tests/golden/make_bench_golden.py."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2410_23317_b200 as V
+from paper_2410_23317_b200.errors import SpecTooLargeError, ValidationError, ZeroVarianceError
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+META = json.load(open(os.path.join(HERE, "golden", "bench_golden.json")))
+
+
+@pytest.fixture(scope="module")
+def bg():
+    return np.load(os.path.join(HERE, "golden", "bench_golden.npz"))
+
+
+def spec(i):
+    policy, budget, alpha = META["cases"][i]
+    return V.BenchSpec(policy=policy, budget=budget, alpha=alpha, **META["base"])
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(prompt_len=0), "prompt_len"), (dict(repeats=2), "repeats"), (dict(alpha=0.0), "alpha"),
+    (dict(alpha=1.5), "alpha"), (dict(policy="lru"), "policy"), (dict(budget="pyramid"), "budget"),
+    (dict(post_vision_len=500), "post_vision_len"), (dict(stats_window=-1), "stats_window"),
+    (dict(threads=0), "threads"), (dict(tile=0), "tile")])
+def test_spec_validation(kw, msg):
+    base = dict(prompt_len=128, post_vision_len=32)
+    base.update(kw)
+    with pytest.raises(ValidationError, match=msg):
+        V.BenchSpec(**base)
+
+
+def test_memory_accounting_matches_reference():
+    s = spec(len(META["cases"]) - 1)
+    assert V.estimate_bytes(s) == META["estimate_bytes"]
+    assert V.kv_cache_bytes([10, 20], s) == 2 * 30 * s.head_dim * 4 * s.num_kv_heads
+    with pytest.raises(SpecTooLargeError):
+        V.run_bench(V.BenchSpec(prompt_len=4096, num_layers=64, num_query_heads=64, max_bytes=1 << 20))
+
+
+def test_threshold_filter_and_curve_similarity():
+    a = np.array([[1.0, 0.5, 0.004, 0.0], [0.2, 0.1, 0.0001, 0.2]])
+    got = V.threshold_filter(a, 0.01)
+    np.testing.assert_array_equal(got, [[1.0, 0.5, 0.0, 0.0], [0.2, 0.1, 0.0, 0.2]])
+    np.testing.assert_array_equal(V.threshold_filter(got, 0.01), got)        # idempotent
+    np.testing.assert_array_equal(V.threshold_filter(a[0], 0.01), got[0])
+    for bad in (np.array([]), np.array([1.0, -1.0]), np.array([np.nan]), np.zeros((1, 1, 1))):
+        with pytest.raises(ValidationError):
+            V.threshold_filter(bad, 0.01)
+    mk = lambda g: V.LayerSparsity(phase="x", p=0.01, gamma=np.asarray(g, dtype=float))  # noqa: E731
+    x = mk([[0.1, 0.3], [0.5, 0.7], [0.2, 0.2]])
+    assert V.curve_similarity(x, x) == pytest.approx(1.0)
+    y = mk([[0.9, 0.7], [0.5, 0.3], [0.8, 0.8]])
+    assert V.curve_similarity(x, y) == pytest.approx(-1.0)
+    with pytest.raises(ZeroVarianceError):
+        V.curve_similarity(x, mk([[0.5, 0.5]] * 3))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(len(META["cases"])))
+def test_gpu_compression_pass_matches_reference(bg, i):
+    """Every policy x budget mode: kept counts and kept index sets equal the
+    reference's compression pass (bench.py:245-323) on the same trace."""
+    from paper_2410_23317_b200.harness import _compression_pass, _setup
+
+    s = spec(i)
+    trace, values, res = _setup(s)
+    alloc, kept, secs = _compression_pass(res, s)
+    np.testing.assert_array_equal(alloc.kept_counts, bg[f"c{i}_kept_counts"])
+    for l in range(s.num_layers):
+        for kv in range(s.num_kv_heads):
+            np.testing.assert_array_equal(kept[l][kv], bg[f"c{i}_kept_{l}_{kv}"], err_msg=f"{i} {l} {kv}")
+    assert secs > 0
+
+
+@pytest.mark.gpu
+def test_gpu_run_bench_report(bg):
+    s = spec(0)
+    rep = V.run_bench(s)
+    assert sorted(rep.to_dict()) == META["report_keys"]
+    assert rep.kept_counts == list(bg["c0_kept_counts"])
+    assert [rep.kv_bytes_full, rep.kv_bytes_compressed] == list(bg["c0_kv"])
+    assert rep.backend == "b200" and len(rep.decode_times_full_s) == s.repeats
+    assert rep.decode_time_full_s > 0 and rep.decode_time_compressed_s > 0 and rep.prefill_time_s > 0
+    rows = V.latency_throughput_curve([s, V.BenchSpec(**{**META["base"], "batch_size": 2})])
+    assert [r["mode"] for r in rows] == ["full", "compressed"] * 2
+    ov = V.stats_overhead(s)
+    assert ov.stats_time_s > 0 and ov.fraction == ov.stats_time_s / ov.prefill_time_s
