@@ -170,6 +170,7 @@ class _Resident:
                 t = torch.nn.functional.pad(t, (0, self.dp - self.d))
             return t.contiguous()
 
+        self.engines = {}                  # (start, end) -> (window engine, its query rows)
         self.q = stack(trace.queries)      # [1, L, Hq, T, dp]
         self.k = stack(trace.keys)         # [1, L, Hkv, T, dp]
         self.v = stack(values)
@@ -189,10 +190,14 @@ def _window_engine(res: _Resident, spec: BenchSpec, start: int, end: int):
     resident tensors: column mass, below counts, gamma and gamma'."""
     from .engine import Shape, VLCache
 
-    shape = Shape(1, spec.num_layers, spec.num_query_heads, spec.num_kv_heads, res.dp, end, end - start)
-    eng = VLCache(shape, alpha=spec.alpha, p=spec.p, recent_frac=spec.recent_window_frac, keep_scores=True,
-                  scale=1.0 / math.sqrt(res.d))
-    eng.score_stats(res.q[:, :, :, start:end].contiguous(), res.k)
+    key = (start, end)
+    if key not in res.engines:   # workspaces allocated once per window, as a server would
+        shape = Shape(1, spec.num_layers, spec.num_query_heads, spec.num_kv_heads, res.dp, end, end - start)
+        eng = VLCache(shape, alpha=spec.alpha, p=spec.p, recent_frac=spec.recent_window_frac, keep_scores=True,
+                      scale=1.0 / math.sqrt(res.d))
+        res.engines[key] = (eng, res.q[:, :, :, start:end].contiguous())
+    eng, q_win = res.engines[key]
+    eng.score_stats(q_win, res.k)
     eng.allocate()
     return eng
 
