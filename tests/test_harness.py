@@ -93,3 +93,64 @@ def test_gpu_run_bench_report(bg):
     assert [r["mode"] for r in rows] == ["full", "compressed"] * 2
     ov = V.stats_overhead(s)
     assert ov.stats_time_s > 0 and ov.fraction == ov.stats_time_s / ov.prefill_time_s
+
+
+# ---------------------------------------------------------------- the reference's own harness checks
+@pytest.mark.gpu
+def test_gpu_acceptance_07_kv_byte_ratio():
+    """reference test_acceptance.py:222-241 (criterion 7)."""
+    from paper_2410_23317_b200.harness import _compression_pass, _setup
+
+    for m in (1000, 8000):
+        s = V.BenchSpec(prompt_len=m, n_output_tokens=8)
+        _, _, res = _setup(s)
+        alloc, kept, _ = _compression_pass(res, s)
+        counts = [int(c) for c in alloc.kept_counts]
+        full, comp = V.kv_cache_bytes([m] * s.num_layers, s), V.kv_cache_bytes(counts, s)
+        per_token = 2 * s.head_dim * 4 * s.num_kv_heads
+        assert full == per_token * m * s.num_layers and comp == per_token * sum(counts)
+        assert all(idx.size == c for row, c in zip(kept, counts) for idx in row)
+        assert 0.095 <= comp / full <= 0.115, (m, comp / full)
+
+
+@pytest.mark.gpu
+def test_gpu_acceptance_08_decode_speedup_trends():
+    """reference test_acceptance.py:244-266 (criterion 8), on the B200."""
+    import time
+
+    t0 = time.perf_counter()
+    reps = {m: V.run_bench(V.BenchSpec(prompt_len=m)) for m in (2048, 8192, 32768)}
+    elapsed = time.perf_counter() - t0
+    sp = [reps[m].decode_speedup for m in (2048, 8192, 32768)]
+    assert reps[8192].decode_speedup > 1.5 and reps[32768].decode_speedup > 2.0, sp
+    inv = [(a, b) for a, b in zip(sp, sp[1:]) if b < a]
+    assert len(inv) <= 1 and all(b >= 0.95 * a for a, b in inv), sp
+    assert all(r.end_to_end_speedup <= r.decode_speedup for r in reps.values())
+    assert elapsed < 600.0
+
+
+@pytest.mark.gpu
+def test_gpu_harness_reference_behaviours():
+    """reference test_bench.py:107-118, 168-203."""
+    from paper_2410_23317_b200.harness import _compression_pass, _setup
+
+    rep = V.run_bench(V.BenchSpec(prompt_len=256, n_output_tokens=4, alpha=1.0, budget="uniform"))
+    assert rep.kept_counts == [256, 256] and rep.kv_bytes_compressed == rep.kv_bytes_full
+    s = V.BenchSpec(prompt_len=256, n_output_tokens=4, policy="streaming", alpha=0.2)
+    _, _, res = _setup(s)
+    _, kept, _ = _compression_pass(res, s)
+    n_init = -(-len(kept[0][0]) // 10)
+    assert set(range(n_init)) <= set(kept[0][0].tolist())
+    s = V.BenchSpec(prompt_len=256, n_output_tokens=4, alpha=0.3)
+    _, _, res = _setup(s)
+    a1, k1, _ = _compression_pass(res, s)
+    a2, k2, _ = _compression_pass(res, s)
+    np.testing.assert_array_equal(a1.kept_counts, a2.kept_counts)
+    assert all(np.array_equal(x, y) for r1, r2 in zip(k1, k2) for x, y in zip(r1, r2))
+    assert all(len(k1[l][kv]) == a1.kept_counts[l] for l in range(2) for kv in range(2))
+    ov = V.stats_overhead(V.BenchSpec(prompt_len=256, n_output_tokens=4, post_vision_len=0, budget="uniform"))
+    assert ov.stats_time_s == 0.0 and ov.fraction == 0.0
+    with pytest.raises(ValidationError, match="prompt_len"):
+        V.latency_throughput_curve([V.BenchSpec(prompt_len=128, post_vision_len=16), V.BenchSpec(prompt_len=256)])
+    with pytest.raises(ValidationError, match="specs"):
+        V.latency_throughput_curve([])
