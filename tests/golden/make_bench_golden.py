@@ -19,6 +19,10 @@ BASE = dict(prompt_len=320, n_output_tokens=4, num_layers=3, num_query_heads=4, 
             post_vision_len=64, stats_window=50, repeats=3, warmup=1, seed=5)
 CASES = [("vlcache", "sparsity_aware", 0.1), ("h2o", "sparsity_aware", 0.1), ("sliding", "uniform", 0.2),
          ("streaming", "uniform", 0.1), ("vlcache", "uniform", 0.3), ("sliding", "sparsity_aware", 0.05)]
+# (policy, budget, alpha, shape overrides): odd head dims, MHA, no post-vision rows
+EXTRA = [("h2o", "uniform", 0.15, dict(head_dim=32, num_query_heads=2, num_kv_heads=2, post_vision_len=0)),
+         ("sliding", "sparsity_aware", 0.1, dict(head_dim=96, post_vision_len=0, stats_window=40)),
+         ("vlcache", "sparsity_aware", 0.25, dict(prompt_len=200, post_vision_len=24, stats_window=50))]
 
 
 def main():
@@ -34,8 +38,8 @@ def main():
 
     rb.generate_trace = rounded
     out, meta = {}, {}
-    for i, (policy, budget, alpha) in enumerate(CASES):
-        spec = rb.BenchSpec(policy=policy, budget=budget, alpha=alpha, **BASE)
+    for i, (policy, budget, alpha, extra) in enumerate([c + ({},) for c in CASES] + EXTRA):
+        spec = rb.BenchSpec(policy=policy, budget=budget, alpha=alpha, **{**BASE, **extra})
         rep = rb.run_bench(spec)
         out[f"c{i}_kept_counts"] = np.array(rep.kept_counts)
         out[f"c{i}_kv"] = np.array([rep.kv_bytes_full, rep.kv_bytes_compressed])
@@ -48,7 +52,7 @@ def main():
         meta["estimate_bytes"] = rb.estimate_bytes(spec)
     np.savez_compressed(os.path.join(HERE, "bench_golden.npz"), **out)
     with open(os.path.join(HERE, "bench_golden.json"), "w") as f:
-        json.dump({"base": BASE, "cases": CASES, **meta}, f, indent=1)
+        json.dump({"base": BASE, "cases": [c + ({},) for c in CASES] + EXTRA, **meta}, f, indent=1)
     print("wrote", len(out), "arrays")
 
 

@@ -21,8 +21,8 @@ def bg():
 
 
 def spec(i):
-    policy, budget, alpha = META["cases"][i]
-    return V.BenchSpec(policy=policy, budget=budget, alpha=alpha, **META["base"])
+    policy, budget, alpha, extra = META["cases"][i]
+    return V.BenchSpec(policy=policy, budget=budget, alpha=alpha, **{**META["base"], **extra})
 
 
 @pytest.mark.parametrize("kw,msg", [
@@ -38,8 +38,8 @@ def test_spec_validation(kw, msg):
 
 
 def test_memory_accounting_matches_reference():
-    s = spec(len(META["cases"]) - 1)
-    assert V.estimate_bytes(s) == META["estimate_bytes"]
+    assert V.estimate_bytes(spec(len(META["cases"]) - 1)) == META["estimate_bytes"]
+    s = spec(0)
     assert V.kv_cache_bytes([10, 20], s) == 2 * 30 * s.head_dim * 4 * s.num_kv_heads
     with pytest.raises(SpecTooLargeError):
         V.run_bench(V.BenchSpec(prompt_len=4096, num_layers=64, num_query_heads=64, max_bytes=1 << 20))
