@@ -134,16 +134,37 @@ def check_kept_sets(got, ref, scores, counts):
     (8, 2, 1200, 64, 128, 56),   # Y34B-style G=7
 ])
 def test_engine_compress_and_decode_match_oracle(hkv, layers, m, tau, d, hq):
-    n_dec = 6
+    run_parity_case(hkv, layers, m, tau, d, hq)
+
+
+def _fuzz_cases(n=24, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        hkv = int(rng.choice([1, 2, 4, 8]))
+        g = int(rng.choice([1, 2, 3, 4, 7, 8]))
+        m = int(rng.integers(64, 1500))
+        out.append((hkv, int(rng.integers(1, 4)), m, int(rng.integers(1, min(m, 160) + 1)),
+                    int(rng.choice([64, 128])), hkv * g, float(rng.uniform(0.02, 0.5)), int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("hkv,layers,m,tau,d,hq,alpha,seed", _fuzz_cases())
+def test_engine_fuzz_matches_oracle(hkv, layers, m, tau, d, hq, alpha, seed):
+    """Random shapes, windows, budgets and seeds through the whole path."""
+    run_parity_case(hkv, layers, m, tau, d, hq, alpha=alpha, seed=seed, n_dec=4)
+
+
+def run_parity_case(hkv, layers, m, tau, d, hq, alpha=0.1, seed=0, n_dec=6):
     spec = GenSpec(num_layers=layers, num_query_heads=hq, num_kv_heads=hkv, head_dim=d, prompt_len=m,
-                   post_vision_len=tau, decode_len=n_dec, seed=0)
+                   post_vision_len=tau, decode_len=n_dec, seed=seed)
     host, dv = make_inputs(spec, tau)
     g = hq // hkv
-    eng = VLCache(Shape(B=1, L=layers, Hq=hq, Hkv=hkv, d=d, m=m, w=tau), decode_steps=n_dec,
+    eng = VLCache(Shape(B=1, L=layers, Hq=hq, Hkv=hkv, d=d, m=m, w=tau), alpha=alpha, decode_steps=n_dec,
                   keep_scores=True)
     eng.compress(dv["q_win"], dv["keys"], dv["values"])
     torch.cuda.synchronize()
-    ref = O.compression_pass(host[0]["q_win"], host[0]["keys"], m, g, tile=128)
+    ref = O.compression_pass(host[0]["q_win"], host[0]["keys"], m, g, tile=128, alpha=alpha)
     below = eng.below_head.view(layers, hq).cpu().numpy()
     ref_below = np.array([[ref["stats"][(l, h)][3].sum() for h in range(hq)] for l in range(layers)])
     np.testing.assert_array_equal(below, ref_below)
