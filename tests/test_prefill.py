@@ -146,3 +146,29 @@ def test_gpu_prefill_compress_random_inputs(B, L, HQ, HKV, D, M, W):
     ka, kb = a.kept_sets(), b.kept_sets()
     for bb in range(B):
         check_kept_sets(kb[bb], ka[bb], scores[bb], counts[bb])
+
+
+def _prefill_fuzz(n=10, seed=77):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        hkv = int(rng.choice([1, 2, 4]))
+        out.append((int(rng.integers(0, 1 << 30)), hkv * int(rng.choice([1, 2, 4, 8])), hkv,
+                    int(rng.choice([16, 32, 64, 80, 128])), int(rng.integers(1, 700))))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed,h,hkv,d,m", _prefill_fuzz())
+def test_gpu_prefill_fuzz(seed, h, hkv, d, m):
+    """Random shapes (odd head dims padded, single-row prompts, GQA) against the
+    oracle's float32 restatement of the reference prefill."""
+    from paper_2410_23317_b200.prefill import prefill_attention
+
+    rng = np.random.default_rng(seed)
+    q = round_to_bf16(rng.standard_normal((h, m + 2, d)).astype(np.float32) * 1.5)
+    k = round_to_bf16(rng.standard_normal((hkv, m + 2, d)).astype(np.float32))
+    v = round_to_bf16(rng.standard_normal((hkv, m + 2, d)).astype(np.float32))
+    got = prefill_attention(q, k, v, m)
+    want = O.prefill_layer(q, k, v, m, 128)
+    np.testing.assert_allclose(got, want, atol=2e-2, rtol=0)
