@@ -6,17 +6,18 @@
 // compression path; PAPER.md:528-553 (the post-vision statistics ride on the
 // prefill's Q K^T).
 //
-// Two passes per CTA = (query head, block of 128 prompt rows), like K1:
-//   pass 1: S = Q K^T tile by tile (TMEM) -> exact row max (thread = row; no exp)
-//   pass 2: S again -> P = 2^(S c1 - max c1) <= 1 as bf16 into tensor memory
-//           (tcgen05.st; two P stages of 64 packed columns) -> O += P V on
-//           tcgen05 with A = P read from TMEM and B = V^T tiles (pre-transposed
-//           once, K-major) from shared memory.  VLC_PF_TS=0 builds the variant
-//           that stages P in shared memory (UMMA A layout, 128-byte swizzle).
-// The row max is final before any P is formed, so O accumulates in TMEM with
-// no rescaling and is divided by the row sum (accumulated alongside P) once at
-// the end; one exponential per entry; the cost is one extra Q K^T (3 MMAs per
-// tile instead of 2) and a max-only first pass.
+// One pass per CTA = (query head, block of 128 prompt rows), online softmax:
+// per 128-key tile, S = Q K^T lands in TMEM; the epilogue (thread = row, four
+// warps per row sharing the tile's columns) takes the tile's row max through
+// shared memory, forms P = 2^(S c1 - m_ref c1) as bf16 into tensor memory
+// (tcgen05.st) and the MMA warp accumulates O += P V in TMEM with A = P from
+// TMEM and B = V^T tiles (pre-transposed once, K-major) from shared memory.
+// m_ref, the reference max, is raised only when the row max grows by more
+// than 2^8; then O's row (tcgen05.ld / scale / tcgen05.st, after the previous
+// P V retired) and the running sum are rescaled.  O / sum at the end; the row
+// statistics emitted are the exact row max and the sum relative to it.
+// VLC_PF_ONEPASS=0 builds the two-pass variant (max-only pass, then P with the
+// final max: a second Q K^T per tile, no rescaling).
 // Warps: 0 K producer, 1 MMA issuer, 2 TMEM allocator, 3 V^T producer,
 // 4-19 epilogue (lane quarter x 32-column group).
 #include <cuda.h>
@@ -37,7 +38,12 @@ constexpr uint32_t kTmemCols = 512;   // S: 2 x 128, O: d <= 128, P (TS mode): 2
 #define VLC_PF_TS 1
 #endif
 constexpr bool kTS = VLC_PF_TS;       // P through TMEM (A operand from tensor memory) instead of smem
-constexpr int kKS = 2;                 // K tile ring (a third stage measured no faster)
+constexpr int kKS = 2;
+#ifndef VLC_PF_ONEPASS
+#define VLC_PF_ONEPASS 1
+#endif
+constexpr bool kOnePass = VLC_PF_ONEPASS;   // online softmax with lazy O rescaling (one Q K^T per tile)
+constexpr int kPasses = kOnePass ? 1 : 2;                 // K tile ring (a third stage measured no faster)
 
 template <int D>
 struct PL {
@@ -76,8 +82,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ uint64_t qfull, kfull[kKS], kempty[kKS], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
         ofull;
     __shared__ uint32_t tmem_slot;
-    __shared__ float c_mb[kM], c_part[4 * kM];
-    float2* rowstat = reinterpret_cast<float2*>(sp);   // [4 * kM], pass 1 only (P is pass 2 only)
+    [[maybe_unused]] __shared__ float c_mb[kM];
+    __shared__ float c_part[4 * kM];
+    [[maybe_unused]] __shared__ float xmax[kOnePass ? 2 : 1][4][kM];      // one-pass: tile row max per column group
+    [[maybe_unused]] float2* rowstat = reinterpret_cast<float2*>(sp);   // [4 * kM], pass 1 only (P is pass 2 only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sq_slot = blockIdx.y;                                  // (b, l, query head)
@@ -115,7 +123,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::mbar_expect_tx(&qfull, LY::kQ);
             for (int kb = 0; kb < LY::KB; ++kb)
                 sm100::tma_load_2d(sq + kb * kM * 128, &qmap, &qfull, kb * 64, (int)(sq_slot * a.q_rows + r0));
-            for (int it = 0; it < 2 * T; ++it) {
+            for (int it = 0; it < kPasses * T; ++it) {
                 const int st = it % kKS, t = it < T ? it : it - T;
                 sm100::mbar_wait(kempty + st, ((it / kKS) & 1) ^ 1);
                 sm100::mbar_expect_tx(kfull + st, LY::kK);
@@ -177,9 +185,10 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 sm100::mma_commit(vempty + st);
             };
             sm100::mbar_wait(&qfull, 0);
-            for (int it = 0; it < T; ++it) qk(it);
+            const int p1 = kOnePass ? 0 : T;
+            for (int it = 0; it < p1; ++it) qk(it);
             for (int t = 0; t < T; ++t) {
-                qk(T + t);
+                qk(p1 + t);
                 if (t > 0) pv(t - 1);
             }
             pv(T - 1);
@@ -197,92 +206,183 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         const float c1 = a.inv_scale * kLog2e;
         float l[32];
 
-        // pass 1: row max of the raw dots only (no exponentials)
-        float m = -INFINITY;
-        for (int it = 0; it < T; ++it) {
-            const int st = it & 1;
-            sm100::mbar_wait(tfull + st, (it >> 1) & 1);
-            sm100::tc_fence_after();
-            sm100::tmem_ld32(lane_addr + st * kN, l);
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tempty + st);
-            const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
-            if (__all_sync(kFull, valid == 32)) {
+        float S, il, row_M;
+        if constexpr (kOnePass) {
+            // one pass: per tile, the row max across the four column groups of the
+            // lane quarter; P uses a reference max m_ref that is only raised when
+            // the row max grows by more than 2^8 (then O and the sum are rescaled)
+            const float grow_raw = 8.f / c1;
+            float m_ref = -INFINITY, m_true = -INFINITY;
+            float ps[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int t = 0; t < T; ++t) {
+                const int st = t & 1, pb = t & 1;
+                sm100::mbar_wait(tfull + st, (t >> 1) & 1);
+                sm100::tc_fence_after();
+                sm100::tmem_ld32(lane_addr + st * kN, l);
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + st);
+                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
+                const bool full = __all_sync(kFull, valid == 32);
+                float cm = -INFINITY;
+                if (full) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) m = fmaxf(m, l[k]);
-            } else {
+                    for (int k = 0; k < 32; ++k) cm = fmaxf(cm, l[k]);
+                } else {
 #pragma unroll
-                for (int k = 0; k < 32; ++k) m = k < valid ? fmaxf(m, l[k]) : m;
-            }
-        }
-        rowstat[cg * kM + li] = make_float2(m, 0.f);
-        sm100::named_bar_sync(1, kEpiWarps * 32);
-        if (cg == 0) {
-            float M = -INFINITY;
-#pragma unroll
-            for (int g = 0; g < 4; ++g) M = fmaxf(M, rowstat[g * kM + li].x);
-            c_mb[li] = row_ok ? M * c1 : 0.f;
-            if (row_ok && a.row_max) a.row_max[(int64_t)sq_slot * a.m + r] = M * a.inv_scale;
-        }
-        sm100::named_bar_sync(1, kEpiWarps * 32);
-        const float mb = c_mb[li];
-
-        // pass 2: P = 2^(l c1 - mb) <= 1 (0 past the causal frontier) as bf16,
-        // the row sum of the same exponentials on the side; O = (P V) / sum at the end
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int t = 0; t < T; ++t) {
-            const int it = T + t, st = it & 1;
-            sm100::mbar_wait(tfull + st, (it >> 1) & 1);
-            sm100::tc_fence_after();
-            sm100::tmem_ld32(lane_addr + st * kN, l);
-            sm100::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(tempty + st);
-            const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
-            uint32_t pk[16];
-            if (__all_sync(kFull, valid == 32)) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const float p0 = ex2(fmaf(l[2 * k], c1, -mb)), p1 = ex2(fmaf(l[2 * k + 1], c1, -mb));
-                    ps[(2 * k) & 3] += p0;
-                    ps[(2 * k + 1) & 3] += p1;
-                    pk[k] = pack_bf16(p0, p1);
+                    for (int k = 0; k < 32; ++k) cm = k < valid ? fmaxf(cm, l[k]) : cm;
                 }
-            } else {
+                xmax[t & 1][cg][li] = cm;
+                sm100::named_bar_sync(2 + sub, 128);                  // the lane quarter's 4 warps
+                const float tm = fmaxf(fmaxf(xmax[t & 1][0][li], xmax[t & 1][1][li]),
+                                       fmaxf(xmax[t & 1][2][li], xmax[t & 1][3][li]));
+                m_true = fmaxf(m_true, tm);
+                const bool grow = tm > m_ref + grow_raw;
+                sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);   // P V of tile t - 2 has read P[pb]
+                if (__any_sync(kFull, grow)) {
+                    const float sc = (grow && m_ref != -INFINITY) ? ex2((m_ref - tm) * c1) : 1.f;
+                    if (t > 0 && cg * 32 < D) {
+                        // O holds the tiles before t once P V of tile t - 1 has retired
+                        sm100::mbar_wait(pempty + (pb ^ 1), ((t - 1) >> 1) & 1);
+                        sm100::tc_fence_after();
+                        float o[32];
+                        const uint32_t oa = tmem_o + (uint32_t(32 * sub) << 16) + cg * 32;
+                        sm100::tmem_ld32(oa, o);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) : 0.f;
-                    const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) : 0.f;
-                    ps[(2 * k) & 3] += p0;
-                    ps[(2 * k + 1) & 3] += p1;
-                    pk[k] = pack_bf16(p0, p1);
+                        for (int k = 0; k < 32; ++k) o[k] *= sc;
+                        sm100::tmem_st32(oa, o);
+                    }
+                    if (grow) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) ps[k] *= sc;
+                        m_ref = tm;
+                    }
                 }
-            }
-            const int pb = t & 1;
-            sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);       // P V of tile t - 2 has read this buffer
-            if constexpr (kTS) {
-                // this warp's 32 keys = 16 packed columns of its lane quarter
+                const float mb = m_ref * c1;
+                uint32_t pk[16];
+                if (full) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = ex2(fmaf(l[2 * k], c1, -mb)), p1 = ex2(fmaf(l[2 * k + 1], c1, -mb));
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) : 0.f;
+                        const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) : 0.f;
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                }
                 sm100::tc_fence_after();
                 sm100::tmem_st16(tmem_p + (uint32_t(32 * sub) << 16) + pb * 64 + cg * 16, pk);
                 sm100::tc_fence_before();
-            } else {
-                uint8_t* pdst = sp + pb * LY::kP;
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    *reinterpret_cast<uint4*>(pdst + swz(kM, li, cg * 4 + q)) =
-                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                sm100::fence_proxy_async();                          // generic writes -> async proxy
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(pfull + pb);
             }
-            __syncwarp();
-            if (lane == 0) sm100::mbar_arrive(pfull + pb);
+            c_part[cg * kM + li] = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+            sm100::named_bar_sync(1, kEpiWarps * 32);
+            const float l_ref = (c_part[li] + c_part[kM + li]) + (c_part[2 * kM + li] + c_part[3 * kM + li]);
+            il = row_ok ? 1.f / l_ref : 0.f;
+            S = l_ref * ex2((m_ref - m_true) * c1);                  // the sum relative to the true max
+            row_M = m_true;
+        } else {
+            // pass 1: row max of the raw dots only (no exponentials)
+            float m = -INFINITY;
+            for (int it = 0; it < T; ++it) {
+                const int st = it & 1;
+                sm100::mbar_wait(tfull + st, (it >> 1) & 1);
+                sm100::tc_fence_after();
+                sm100::tmem_ld32(lane_addr + st * kN, l);
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + st);
+                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)it * kN + cg * 32)));
+                if (__all_sync(kFull, valid == 32)) {
+    #pragma unroll
+                    for (int k = 0; k < 32; ++k) m = fmaxf(m, l[k]);
+                } else {
+    #pragma unroll
+                    for (int k = 0; k < 32; ++k) m = k < valid ? fmaxf(m, l[k]) : m;
+                }
+            }
+            rowstat[cg * kM + li] = make_float2(m, 0.f);
+            sm100::named_bar_sync(1, kEpiWarps * 32);
+            if (cg == 0) {
+                float M = -INFINITY;
+    #pragma unroll
+                for (int g = 0; g < 4; ++g) M = fmaxf(M, rowstat[g * kM + li].x);
+                c_mb[li] = row_ok ? M * c1 : 0.f;
+                if (row_ok && a.row_max) a.row_max[(int64_t)sq_slot * a.m + r] = M * a.inv_scale;
+            }
+            sm100::named_bar_sync(1, kEpiWarps * 32);
+            const float mb = c_mb[li];
+
+            // pass 2: P = 2^(l c1 - mb) <= 1 (0 past the causal frontier) as bf16,
+            // the row sum of the same exponentials on the side; O = (P V) / sum at the end
+            float ps[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int t = 0; t < T; ++t) {
+                const int it = T + t, st = it & 1;
+                sm100::mbar_wait(tfull + st, (it >> 1) & 1);
+                sm100::tc_fence_after();
+                sm100::tmem_ld32(lane_addr + st * kN, l);
+                sm100::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(tempty + st);
+                const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
+                uint32_t pk[16];
+                if (__all_sync(kFull, valid == 32)) {
+    #pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = ex2(fmaf(l[2 * k], c1, -mb)), p1 = ex2(fmaf(l[2 * k + 1], c1, -mb));
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                } else {
+    #pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) : 0.f;
+                        const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) : 0.f;
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                }
+                const int pb = t & 1;
+                sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);       // P V of tile t - 2 has read this buffer
+                if constexpr (kTS) {
+                    // this warp's 32 keys = 16 packed columns of its lane quarter
+                    sm100::tc_fence_after();
+                    sm100::tmem_st16(tmem_p + (uint32_t(32 * sub) << 16) + pb * 64 + cg * 16, pk);
+                    sm100::tc_fence_before();
+                } else {
+                    uint8_t* pdst = sp + pb * LY::kP;
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        *reinterpret_cast<uint4*>(pdst + swz(kM, li, cg * 4 + q)) =
+                            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    sm100::fence_proxy_async();                          // generic writes -> async proxy
+                }
+                __syncwarp();
+                if (lane == 0) sm100::mbar_arrive(pfull + pb);
+            }
+            // row sums: the four column groups' partials in a fixed order
+            c_part[cg * kM + li] = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+            sm100::named_bar_sync(1, kEpiWarps * 32);
+            S = (c_part[li] + c_part[kM + li]) + (c_part[2 * kM + li] + c_part[3 * kM + li]);
+            if (cg == 0 && row_ok && a.row_sum) a.row_sum[(int64_t)sq_slot * a.m + r] = S;
+            il = row_ok ? 1.f / S : 0.f;
+            row_M = 0.f;   // written in pass 1
         }
-        // row sums: the four column groups' partials in a fixed order
-        c_part[cg * kM + li] = (ps[0] + ps[1]) + (ps[2] + ps[3]);
-        sm100::named_bar_sync(1, kEpiWarps * 32);
-        const float S = (c_part[li] + c_part[kM + li]) + (c_part[2 * kM + li] + c_part[3 * kM + li]);
-        if (cg == 0 && row_ok && a.row_sum) a.row_sum[(int64_t)sq_slot * a.m + r] = S;
-        const float il = row_ok ? 1.f / S : 0.f;
+        if (kOnePass && cg == 0 && row_ok && a.row_max) {
+            a.row_max[(int64_t)sq_slot * a.m + r] = row_M * a.inv_scale;
+            a.row_sum[(int64_t)sq_slot * a.m + r] = S;
+        }
 
         // O: thread = row, warp cg holds dims 32 cg .. 32 cg + 31
         sm100::mbar_wait(&ofull, 0);

@@ -34,7 +34,7 @@ flops = 4 * D * causal * HQ * L * B            # QK^T + PV, the attention's own 
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
 tc = peak.get("bf16_tflops")
 line = {"prefill_ms": ms, "attention_tflops": flops / ms / 1e9, "flops": flops,
-        "issued_tflops": 1.5 * flops / ms / 1e9, "note": "two-pass: 3 MMAs per tile (QK^T twice)"}
+        "note": "one pass (online softmax, lazy O rescale in TMEM): QK^T and PV once per tile"}
 if tc:
     line["frac_of_bf16_peak"] = flops / ms / 1e9 / tc
 # row f2's fusion at the bench workload (generator inputs): prefill + K1 column pass
