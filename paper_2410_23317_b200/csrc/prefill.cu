@@ -43,7 +43,15 @@ constexpr int kKS = 2;
 #define VLC_PF_ONEPASS 1
 #endif
 constexpr bool kOnePass = VLC_PF_ONEPASS;   // online softmax with lazy O rescaling (one Q K^T per tile)
-constexpr int kPasses = kOnePass ? 1 : 2;                 // K tile ring (a third stage measured no faster)
+constexpr int kPasses = kOnePass ? 1 : 2;
+#ifndef VLC_PF_S3
+#define VLC_PF_S3 1
+#endif
+// one pass through TMEM: three S stages with P written over its own S stage
+// (the lane quarter's max exchange already orders every S load before the P
+// store), the stage freed by the P V MMA; S runs two tiles ahead of the epilogue
+constexpr bool kS3 = kOnePass && kTS && VLC_PF_S3;
+constexpr int kSSt = kS3 ? 3 : 2;                 // K tile ring (a third stage measured no faster)
 
 template <int D>
 struct PL {
@@ -79,7 +87,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     uint8_t* sk = sq + LY::kQ;
     uint8_t* sv = sk + kKS * LY::kK;
     uint8_t* sp = sv + 2 * LY::kV;
-    __shared__ uint64_t qfull, kfull[kKS], kempty[kKS], vfull[2], vempty[2], tfull[2], tempty[2], pfull[2], pempty[2],
+    __shared__ uint64_t qfull, kfull[kKS], kempty[kKS], vfull[2], vempty[2], tfull[kSSt], tempty[kSSt], pfull[kSSt], pempty[2],
         ofull;
     __shared__ uint32_t tmem_slot;
     [[maybe_unused]] __shared__ float c_mb[kM];
@@ -98,11 +106,12 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     if (threadIdx.x == 0) {
         sm100::mbar_init(&qfull, 1);
         for (int i = 0; i < kKS; ++i) { sm100::mbar_init(kfull + i, 1); sm100::mbar_init(kempty + i, 1); }
-        for (int i = 0; i < 2; ++i) {
-            sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1);
-            sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kEpiWarps);
+        for (int i = 0; i < 2; ++i) { sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1); }
+        for (int i = 0; i < kSSt; ++i) {   // kS3: the S stage is freed by the P V MMA (one commit)
+            sm100::mbar_init(tfull + i, 1); sm100::mbar_init(tempty + i, kS3 ? 1 : kEpiWarps);
+            sm100::mbar_init(pfull + i, kEpiWarps);
         }
-        for (int i = 0; i < 2; ++i) { sm100::mbar_init(pfull + i, kEpiWarps); sm100::mbar_init(pempty + i, 1); }
+        for (int i = 0; i < 2; ++i) sm100::mbar_init(pempty + i, 1);
         sm100::mbar_init(&ofull, 1);
         sm100::fence_barrier_init();
     }
@@ -111,7 +120,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __syncthreads();
     sm100::tc_fence_after();
     const uint32_t tmem = tmem_slot;
-    const uint32_t tmem_o = tmem + 2 * kN;
+    const uint32_t tmem_o = tmem + (kS3 ? 3 : 2) * kN;
     const uint32_t tmem_p = tmem + 3 * kN;                            // TS mode: P stages, 64 columns each
 
     if (warp < 4) {
@@ -185,6 +194,47 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 sm100::mma_commit(vempty + st);
             };
             sm100::mbar_wait(&qfull, 0);
+            if constexpr (kS3) {
+                auto qk3 = [&](int t) {   // S stage t % 3, free once P V of tile t - 3 retired
+                    const int st = t % 3, ks = t % kKS;
+                    sm100::mbar_wait(tempty + st, ((t / 3) & 1) ^ 1);
+                    sm100::mbar_wait(kfull + ks, (t / kKS) & 1);
+                    sm100::tc_fence_after();
+                    const uint32_t k_addr = sm100::smem_u32(sk + ks * LY::kK);
+#pragma unroll
+                    for (int kb = 0; kb < LY::KB; ++kb)
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            sm100::mma_bf16(tmem + st * kN, sm100::sdesc_k_sw128(q_addr + kb * kM * 128 + kk * 32),
+                                            sm100::sdesc_k_sw128(k_addr + kb * kN * 128 + kk * 32), idesc_s,
+                                            (kb | kk) != 0);
+                    sm100::mma_commit(kempty + ks);
+                    sm100::mma_commit(tfull + st);
+                };
+                auto pv3 = [&](int t) {   // O += P V, P packed over the first 64 columns of S stage t % 3
+                    const int st = t % 3, vs = t & 1;
+                    sm100::mbar_wait(pfull + st, (t / 3) & 1);
+                    sm100::mbar_wait(vfull + vs, (t >> 1) & 1);
+                    sm100::tc_fence_after();
+                    const uint32_t v_addr = sm100::smem_u32(sv + vs * LY::kV);
+#pragma unroll
+                    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            sm100::mma_bf16_ts(tmem_o, tmem + st * kN + (kb * 4 + kk) * 8,
+                                               sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32), idesc_o,
+                                               (t | kb | kk) != 0);
+                    sm100::mma_commit(vempty + vs);
+                    sm100::mma_commit(tempty + st);
+                };
+                qk3(0);
+                if (T > 1) qk3(1);
+                for (int t = 0; t < T; ++t) {
+                    pv3(t);
+                    if (t + 2 < T) qk3(t + 2);
+                }
+                sm100::mma_commit(&ofull);
+            } else {
             const int p1 = kOnePass ? 0 : T;
             for (int it = 0; it < p1; ++it) qk(it);
             for (int t = 0; t < T; ++t) {
@@ -193,6 +243,7 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             }
             pv(T - 1);
             sm100::mma_commit(&ofull);
+            }
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n");
@@ -215,13 +266,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             float m_ref = -INFINITY, m_true = -INFINITY;
             float ps[4] = {0.f, 0.f, 0.f, 0.f};
             for (int t = 0; t < T; ++t) {
-                const int st = t & 1, pb = t & 1;
-                sm100::mbar_wait(tfull + st, (t >> 1) & 1);
+                const int st = kS3 ? t % 3 : t & 1, pb = t & 1;
+                sm100::mbar_wait(tfull + st, (kS3 ? t / 3 : t >> 1) & 1);
                 sm100::tc_fence_after();
                 sm100::tmem_ld32(lane_addr + st * kN, l);
                 sm100::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(tempty + st);
+                if (!kS3 && lane == 0) sm100::mbar_arrive(tempty + st);
                 const int valid = (int)imax(0, imin(32, row_end - ((int64_t)t * kN + cg * 32)));
                 const bool full = __all_sync(kFull, valid == 32);
                 float cm = -INFINITY;
@@ -238,12 +289,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                                        fmaxf(xmax[t & 1][2][li], xmax[t & 1][3][li]));
                 m_true = fmaxf(m_true, tm);
                 const bool grow = tm > m_ref + grow_raw;
-                sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);   // P V of tile t - 2 has read P[pb]
+                if (!kS3) sm100::mbar_wait(pempty + pb, ((t >> 1) & 1) ^ 1);   // P V of tile t - 2 has read P[pb]
                 if (__any_sync(kFull, grow)) {
                     const float sc = (grow && m_ref != -INFINITY) ? ex2((m_ref - tm) * c1) : 1.f;
                     if (t > 0 && cg * 32 < D) {
                         // O holds the tiles before t once P V of tile t - 1 has retired
-                        sm100::mbar_wait(pempty + (pb ^ 1), ((t - 1) >> 1) & 1);
+                        if constexpr (kS3) sm100::mbar_wait(tempty + (t - 1) % 3, ((t - 1) / 3) & 1);
+                        else sm100::mbar_wait(pempty + (pb ^ 1), ((t - 1) >> 1) & 1);
                         sm100::tc_fence_after();
                         float o[32];
                         const uint32_t oa = tmem_o + (uint32_t(32 * sub) << 16) + cg * 32;
@@ -279,10 +331,13 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     }
                 }
                 sm100::tc_fence_after();
-                sm100::tmem_st16(tmem_p + (uint32_t(32 * sub) << 16) + pb * 64 + cg * 16, pk);
+                if constexpr (kS3)   // over this tile's own S stage (all of its S loads are done)
+                    sm100::tmem_st16(tmem + (uint32_t(32 * sub) << 16) + st * kN + cg * 16, pk);
+                else
+                    sm100::tmem_st16(tmem_p + (uint32_t(32 * sub) << 16) + pb * 64 + cg * 16, pk);
                 sm100::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) sm100::mbar_arrive(pfull + pb);
+                if (lane == 0) sm100::mbar_arrive(pfull + (kS3 ? st : pb));
             }
             c_part[cg * kM + li] = (ps[0] + ps[1]) + (ps[2] + ps[3]);
             sm100::named_bar_sync(1, kEpiWarps * 32);
