@@ -237,6 +237,26 @@ def k1_flops(batch):
     return 2 * c["head_dim"] * c["q_heads"] * causal * c["layers"] * batch
 
 
+def k1_mufu_floor(batch, torch):
+    """ex2 count of K1 (two per causal entry: row pass and column pass) over the
+    device's SFU rate at its max SM clock: the epilogue's floor in microseconds."""
+    c = CFG
+    m, tau = c["prompt_len"], c["tau"]
+    exps = 2 * (tau * (m - tau) + tau * (tau + 1) // 2) * c["q_heads"] * c["layers"] * batch
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    sms = props.multi_processor_count
+    mhz = None
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        mhz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()),
+                                               pynvml.NVML_CLOCK_SM)
+    except Exception:  # noqa: BLE001
+        mhz = 1965
+    return {"exps": exps, "floor_us": exps / (sms * 16 * mhz * 1e6) * 1e6}
+
+
 def run_gpu_arm(args):
     import torch
     import torch.distributed as dist
@@ -381,6 +401,9 @@ def run_gpu_arm(args):
         "k1_ms": k1_ms, "k234_ms": float(np.mean(k234)), "decode_ms_99_steps": dec_ms,
         "decode_tokens_per_s": B * n_dec * world / (dec_ms / 1e3),
         "k1_tensor_tflops": k1_tflops, "k1_tensor_frac": k1_tflops / tc_peak,
+        # K1's binding floor is its epilogue: two ex2 per causal entry on the SFU
+        # (16 lanes / SM / clock on sm_100); exact mode's fix-ups included in k1_ms
+        "k1_mufu": k1_mufu_floor(B, torch),
         "roofline": roof,
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
@@ -389,6 +412,7 @@ def run_gpu_arm(args):
         "clocks": clk.summary(),
         "kept_tokens_per_layer_mean": float(counts.mean()),
     }
+    line["k1_mufu"]["frac"] = line["k1_mufu"]["floor_us"] / (k1_ms * 1e3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         kind = cpu_kind()
