@@ -131,7 +131,6 @@ def test_head_sharded_budgets_equal_unsharded():
     """KV-head sharding (parallel.HeadShard): each 'rank' runs K1 on its KV
     heads only; the zero-padded int64 counts summed over ranks (what the NCCL
     all-reduce does) give bit-identical budgets and kept sets to one device."""
-    from paper_2410_23317_b200 import _lib
     from paper_2410_23317_b200.parallel import HeadShard
 
     L, HQ, HKV, D, M, TAU, WORLD = 2, 56, 8, 128, 1500, 64, 4
