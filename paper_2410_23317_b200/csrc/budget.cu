@@ -45,6 +45,7 @@ __device__ double pairwise_sum(const double* a, int64_t n, int64_t stride) {
 constexpr int kAllocThreads = 1024;
 
 __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(BudgetArgs a) {
+    pdl_wait_then_release();
     __shared__ long long scan_k[32], scan_c[32];
     const int64_t BL = (int64_t)a.B * a.L;
     if (a.below_head) {
@@ -114,8 +115,7 @@ __global__ void __launch_bounds__(kAllocThreads) allocate_kernel(BudgetArgs a) {
 
 cudaError_t launch_allocate(const BudgetArgs& a, cudaStream_t st) {
     if (a.B > 1024) return cudaErrorInvalidValue;
-    allocate_kernel<<<1, kAllocThreads, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(allocate_kernel, dim3(1), dim3(kAllocThreads), 0, st, a);
 }
 
 }  // namespace vlc

@@ -12,6 +12,7 @@ namespace vlc {
 namespace {
 
 __global__ void __launch_bounds__(256) gather_kernel(GatherArgs a) {
+    pdl_wait_then_release();
     const int64_t total_rows = a.kept_off[a.slots];
     const int pieces = a.d / 8;   // 8 bf16 per 16-byte piece
     const int64_t total = total_rows * pieces;
@@ -39,8 +40,7 @@ cudaError_t launch_gather(const GatherArgs& a, cudaStream_t st) {
     const int64_t total = a.max_rows * (a.d / 8);
     int blocks = (int)imin((total + 255) / 256, 148 * 16);
     if (blocks < 1) blocks = 1;
-    gather_kernel<<<blocks, 256, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(gather_kernel, dim3(blocks), dim3(256), 0, st, a);
 }
 
 }  // namespace vlc

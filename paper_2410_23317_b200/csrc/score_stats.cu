@@ -65,6 +65,7 @@ VLC_DEV void add_below(const ScoreArgs& a, const int4& e) {
 // exact logit travels in the waiting entry's .w (its weight is always 1).
 template <int D>
 __global__ void fix_flags(ScoreArgs a) {
+    pdl_wait_then_release();
     const int n = min(a.fix_counts[1], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -114,6 +115,7 @@ VLC_DEV float exact_dot(const uint4* q, const uint4* k, double inv) {
 // its error bound get the float64 dot.
 template <int D>
 __global__ void __launch_bounds__(256) fix_rowscan(ScoreArgs a) {
+    pdl_wait_then_release();
     constexpr int kLanes = D / 8;                 // lanes per key: 16 B each
     constexpr int kPerWarp = 32 / kLanes;         // keys per warp and step
     constexpr float kRel = (float)(D + 4) * 5.9604645e-8f;
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(256) fix_rowscan(ScoreArgs a) {
 // 2b: the row scan's candidates, one float64 dot per thread
 template <int D>
 __global__ void fix_rowmax(ScoreArgs a) {
+    pdl_wait_then_release();
     const int n = min(a.fix_counts[4], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -188,6 +191,7 @@ __global__ void fix_rowmax(ScoreArgs a) {
 // 3: the waiting entries against the exact row max, which also replaces the
 // fp32 row max of those rows
 __global__ void fix_deferred(ScoreArgs a) {
+    pdl_wait_then_release();
     const int n = min(a.fix_counts[0], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
     const int stride = gridDim.x * blockDim.x;
@@ -203,11 +207,12 @@ __global__ void fix_deferred(ScoreArgs a) {
 }
 
 template <int D>
-void launch_fixups(const ScoreArgs& a, cudaStream_t st) {
-    fix_flags<D><<<296, 256, 0, st>>>(a);
-    fix_rowscan<D><<<dim3(24, 148), 256, 0, st>>>(a);
-    fix_rowmax<D><<<296, 256, 0, st>>>(a);
-    fix_deferred<<<148, 256, 0, st>>>(a);
+cudaError_t launch_fixups(const ScoreArgs& a, cudaStream_t st) {
+    cudaError_t e = launch_pdl(fix_flags<D>, dim3(296), dim3(256), 0, st, a);
+    if (e == cudaSuccess) e = launch_pdl(fix_rowscan<D>, dim3(24, 148), dim3(256), 0, st, a);
+    if (e == cudaSuccess) e = launch_pdl(fix_rowmax<D>, dim3(296), dim3(256), 0, st, a);
+    if (e == cudaSuccess) e = launch_pdl(fix_deferred, dim3(148), dim3(256), 0, st, a);
+    return e;
 }
 
 }  // namespace
@@ -235,9 +240,8 @@ cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st) {
     }
     e = launch_score_stats_tc(a, score_partials((int64_t)a.G * a.w), st);
     if (e != cudaSuccess || a.cap <= 0) return e;
-    if (a.d == 64) launch_fixups<64>(a, st);
-    else launch_fixups<128>(a, st);
-    return cudaGetLastError();
+    e = a.d == 64 ? launch_fixups<64>(a, st) : launch_fixups<128>(a, st);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace vlc

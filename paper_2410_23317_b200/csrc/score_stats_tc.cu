@@ -108,6 +108,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ int c_lim[kM];                           // last visible key (-1: no row)
     __shared__ int hcnt[kM];                            // below counts per head of the block
 
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the fix-ups wait for completion
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // CTA -> (slot s, row block rb, key part).  The first n_full CTAs take whole
     // units; the rest -- the units of the last, partial wave -- come in pairs

@@ -27,6 +27,7 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
 }
 
 __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
+    pdl_wait_then_release();
     extern __shared__ unsigned long long keys_smem[];
     __shared__ unsigned int hist[256];
     __shared__ long long scan_scratch[32];
@@ -177,8 +178,7 @@ cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.n > kSmemKeysMax && !a.key_scratch) return cudaErrorInvalidValue;  // needs global scratch
     const size_t sm = a.n <= kSmemKeysMax ? sizeof(unsigned long long) * (size_t)a.n : 0;
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemKeysMax * 8));
-    select_kernel<<<a.slots, kThreads, sm, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(select_kernel, dim3(a.slots), dim3(kThreads), sm, st, a);
 }
 
 }  // namespace vlc
