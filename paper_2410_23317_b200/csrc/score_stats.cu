@@ -226,18 +226,28 @@ int exact_ws_cap(int64_t bytes, int64_t slots, int64_t rows) {
     return (int)(cap > (1 << 30) ? (1 << 30) : cap);
 }
 
+// the count outputs and exact mode's counters / row keys, zeroed in one launch
+__global__ void zero_outputs(unsigned* p0, int64_t n0, unsigned* p1, int64_t n1, unsigned* p2, int64_t n2,
+                             unsigned* p3, int64_t n3) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2 + n3; i += stride) {
+        if (i < n0) p0[i] = 0u;
+        else if (i < n0 + n1) p1[i - n0] = 0u;
+        else if (i < n0 + n1 + n2) p2[i - n0 - n1] = 0u;
+        else p3[i - n0 - n1 - n2] = 0u;
+    }
+}
+
 cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(a.below_head, 0, sizeof(unsigned long long) * a.slots * a.G, st);
+    const int64_t nh = 2 * (int64_t)a.slots * a.G;                       // u64 below_head
+    const int64_t nc = a.below_col ? (int64_t)a.slots * a.n : 0;
+    const int64_t nf = a.cap > 0 ? 8 : 0, nr = a.cap > 0 ? (int64_t)a.slots * a.G * a.w : 0;
+    const int64_t tot = nh + nc + nf + nr;
+    zero_outputs<<<(unsigned)imin(4 * 148, (tot + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<unsigned*>(a.below_head), nh, reinterpret_cast<unsigned*>(a.below_col), nc,
+        reinterpret_cast<unsigned*>(a.fix_counts), nf, a.rmax_key, nr);
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (a.below_col) {
-        e = cudaMemsetAsync(a.below_col, 0, sizeof(int) * a.slots * a.n, st);
-        if (e != cudaSuccess) return e;
-    }
-    if (a.cap > 0) {
-        e = cudaMemsetAsync(a.fix_counts, 0, 8 * sizeof(int), st);
-        if (e == cudaSuccess) e = cudaMemsetAsync(a.rmax_key, 0, sizeof(unsigned) * a.slots * a.G * a.w, st);
-        if (e != cudaSuccess) return e;
-    }
     e = launch_score_stats_tc(a, score_partials((int64_t)a.G * a.w), st);
     if (e != cudaSuccess || a.cap <= 0) return e;
     e = a.d == 64 ? launch_fixups<64>(a, st) : launch_fixups<128>(a, st);
