@@ -244,3 +244,45 @@ def test_gpu_batched_head_scores_bit_identical(tau, group):
     rep = V.build_report(tr, {"pv": V.PostVision()}, k=50).to_dict()
     for row in rep["hit_rates"]:
         assert row["hit_rate"] == V.cache_hit_rate(tr, row["layer"], row["head"], V.PostVision(), 50)
+
+
+def _eval_fuzz(n=8, seed=99):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        hkv = int(rng.choice([1, 2, 4]))
+        m = int(rng.integers(40, 500))
+        out.append(dict(num_layers=1, num_query_heads=hkv * int(rng.choice([1, 2, 4])), num_kv_heads=hkv,
+                        head_dim=int(rng.choice([16, 32, 48, 64])), prompt_len=m,
+                        post_vision_len=int(rng.integers(0, m // 2)), decode_len=int(rng.integers(1, 6)),
+                        seed=int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", _eval_fuzz())
+def test_gpu_eval_fuzz(spec):
+    """Random shapes (odd head dims, MHA/GQA, short prompts, tau = 0) against the
+    oracle restatement: contribution within float32-exp rounding, coverage and
+    hit rates within one position of a near-tie per row."""
+    import paper_2410_23317_b200 as V
+
+    tr, _ = generate_trace(GenSpec(**spec))
+    h = tr.header
+    m, seq = h.prompt_len, h.seq_len
+    win = V.EvalWindow.for_header(h, alpha_eval=0.2)
+    k = max(1, m // 10)
+    for q in range(h.num_query_heads):
+        kv = tr.kv_head_for(q)
+        probs = O.causal_probs(tr.queries[0][q, m:seq], tr.keys[0][kv, :seq], m, seq)
+        for mod in ("vision", "language"):
+            idx = tr.layout.indices(mod)
+            want = O.filtered_share(probs, m, idx, 0.01) if idx.size else 0.0
+            assert V.contribution(tr, 0, q, win, mod) == pytest.approx(want, rel=1e-6, abs=1e-12)
+            if win.top_k <= m:
+                cov = V.coverage(tr, 0, q, win, mod)
+                assert abs(cov - O.topk_share(probs, m, idx, win.top_k)) <= 1.0 / win.top_k + 1e-12
+        orow = O.causal_probs(tr.queries[0][q, m:m + 1], tr.keys[0][kv, :m], m, m)
+        np.testing.assert_allclose(V.oracle_scores(tr, 0, q), orow[0], rtol=1e-6, atol=1e-300)
+        hr = V.cache_hit_rate(tr, 0, q, orow[0], k)
+        assert hr >= 1.0 - 1.0 / k
