@@ -246,7 +246,11 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 float acc_s[4] = {0.f, 0.f, 0.f, 0.f};   // four chains: ILP for the adds
                 if (full_chunk) {
 #pragma unroll
+#ifdef VLC_K1_NOEX2_TEST
+                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += fmaf(fmaf(l[k], c1, -mb), 0.01f, 1.f);
+#else
                     for (int k = 0; k < kSub; ++k) acc_s[k & 3] += ex2(fmaf(l[k], c1, -mb));
+#endif
                 } else {
 #pragma unroll
                     for (int k = 0; k < kSub; ++k) acc_s[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
@@ -340,7 +344,11 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                         const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
                         cf[e & 1] += u < t2lo ? 1.f : 0.f;
                         if (EXACT) ch[e & 1] += u < t2c + band ? 1.f : 0.f;
+#ifdef VLC_K1_NOEX2_TEST   // timing probe only: is K1 bound by the SFU?
+                        cs[e] = fmaf(fmaf(u, 0.01f, 1.f), ivv[e], cs[e]);
+#else
                         cs[e] = fmaf(ex2(u), ivv[e], cs[e]);
+#endif
                     }
                 }
             } else {
