@@ -408,7 +408,7 @@ def run_gpu_arm(args):
         "e2e": {"value": e2e_value, "unit": "tok/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "path": "VLCache.run_from_host: pinned host inputs; values pulled zero-copy (kept rows only)"},
-        "gpu_launches": args.steps * (8 + n_dec),   # K1 + 4 exact fix-ups, K2, K3, K4, 99 x K5
+        "gpu_launches": args.steps * (9 + n_dec),   # zeroing, K1, 4 exact fix-ups, K2, K3, K4, 99 x K5
         "clocks": clk.summary(),
         "kept_tokens_per_layer_mean": float(counts.mean()),
     }
