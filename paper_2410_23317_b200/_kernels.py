@@ -58,13 +58,24 @@ def stats_tiled(q, keys, q_base, p, tile):
     # p == 1 is accepted by the reference kernel (test_kernels.py:271-277):
     # "below 1.0" equals "below the largest double under 1.0" for float exps
     p_eff = min(float(p), math.nextafter(1.0, 0.0))
-    # exact mode: counts and row max decided like the reference's float64 dots
-    ws_bytes = int(_lib.load().vlc_score_exact_bytes(1, 1, w, w * n + 1024))
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
-    _lib.call("vlc_score_stats", qd.data_ptr(), kd.data_ptr(), 1, 1, dp, n, n, w, int(q_base), p_eff,
-              1.0 / math.sqrt(d), row_max.data_ptr(), row_sum.data_ptr(), col.data_ptr(),
-              below_head.data_ptr(), below_col.data_ptr(), ws.data_ptr(), ws_bytes,
-              torch.cuda.current_stream().cuda_stream)
+    # exact mode: counts and row max decided like the reference's float64 dots.
+    # The re-decision list starts at O(w + 64K) entries (not O(w * n)); on the
+    # rare overflow the call is repeated with room for every listed entry.
+    cap = max(1 << 16, 8 * w)
+    while True:
+        ws_bytes = int(_lib.load().vlc_score_exact_bytes(1, 1, w, cap))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+        below_head.zero_()
+        below_col.zero_()
+        _lib.call("vlc_score_stats", qd.data_ptr(), kd.data_ptr(), 1, 1, dp, n, n, w, int(q_base), p_eff,
+                  1.0 / math.sqrt(d), row_max.data_ptr(), row_sum.data_ptr(), col.data_ptr(),
+                  below_head.data_ptr(), below_col.data_ptr(), ws.data_ptr(), ws_bytes,
+                  torch.cuda.current_stream().cuda_stream)
+        counters = ws[:20].view(torch.int32).cpu().tolist()   # [deferred, listed, overflow, ...]
+        if counters[2] == 0:
+            break
+        cap = max(2 * cap, counters[1] + 1024)
+        del ws
     col_score = col.view(nrb, n).double().sum(0)
     return (row_max.cpu().numpy(), row_sum.double().cpu().numpy(), col_score.cpu().numpy(),
             below_col.long().cpu().numpy(), causal_per_column(n, int(q_base), w))

@@ -21,12 +21,14 @@ Tensors (bf16, CUDA, contiguous):
 from __future__ import annotations
 
 import math
+from collections import OrderedDict
 from dataclasses import dataclass
 
 from . import _lib
-from .errors import DegenerateSparsityError, ValidationError
+from .errors import DegenerateSparsityError, ExactnessError, ValidationError
 
 _ROW_BLOCK = 128  # K1 rows per CTA; col_partial has 2 partials (64-row halves) per block
+_MAX_GRAPHS = 16  # captured decode graphs kept per engine (least recently used evicted)
 
 
 def _ptr(t) -> int:
@@ -95,7 +97,7 @@ class VLCache:
 
     def __init__(self, shape: Shape, *, alpha=0.1, p=0.01, recent_frac=0.10, beta_min=0.01,
                  beta_max=1.0, decode_steps=0, keep_scores=False, device=None, head_shard=None,
-                 scale=None, exact=True):
+                 scale=None, exact=True, exact_capacity=None):
         torch = _lib.require_cuda()
         if not 0.0 < alpha <= 1.0:
             raise ValidationError(f"alpha: must be in (0, 1], got {alpha}")
@@ -144,9 +146,14 @@ class VLCache:
         self.v_cache = torch.zeros(self.cache_rows * s.d, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty(s.B * s.L * s.Hq * s.d, dtype=f32, device=dev)
         # K1 exact mode (vlc.h): room for one listed entry per window row and slot
-        self.exact_ws_bytes = int(_lib.load().vlc_score_exact_bytes(s.slots, s.G, s.w, max(1 << 16, s.slots * R)))
+        # by default; an overflow falls back to fp32 decisions and check() raises
+        cap = max(1 << 16, s.slots * R) if exact_capacity is None else int(exact_capacity)
+        if cap < 1:
+            raise ValidationError(f"exact_capacity: must be >= 1, got {cap}")
+        self.exact_capacity = cap
+        self.exact_ws_bytes = int(_lib.load().vlc_score_exact_bytes(s.slots, s.G, s.w, cap))
         self.exact_ws = torch.empty(self.exact_ws_bytes, dtype=torch.uint8, device=dev) if exact else None
-        self._graphs = {}
+        self._graphs = OrderedDict()
 
     # ------------------------------------------------------------ stages
     def _check_inputs(self, q_win, keys, values=None):
@@ -223,6 +230,10 @@ class VLCache:
                 raise ValidationError(f"{name}: must be a contiguous bf16 CUDA or pinned host tensor")
             if t.dim() != 5 or tuple(t.shape[:3]) != (s.B, s.L, s.Hkv) or t.shape[4] != s.d:
                 raise ValidationError(f"{name}: expected [B, L, Hkv, T, d], got {tuple(t.shape)}")
+        if tuple(values.shape) != tuple(keys.shape):
+            raise ValidationError(f"values: shape {tuple(values.shape)} must match keys {tuple(keys.shape)}")
+        if keys.shape[3] < s.m:
+            raise ValidationError(f"keys: T = {keys.shape[3]} < prompt_len {s.m}")
 
     def score_stats_given(self, q_win, keys, stat_max, stat_sum):
         """K1's column pass only, with the window rows' softmax statistics from the
@@ -280,6 +291,7 @@ class VLCache:
         s = self.shape
         if not 0 <= step < self.decode_steps:
             raise ValidationError(f"step: must be in [0, {self.decode_steps}), got {step}")
+        self._check_decode_inputs(q_dec, keys, values)
         n_dec, T = q_dec.shape[3], keys.shape[3]
         r0 = s.m if row0 is None else int(row0)
         if step >= n_dec or r0 + step >= T:
@@ -291,6 +303,22 @@ class VLCache:
                   _ptr(self.kept_counts), step, s.B, s.L, s.Hkv, s.G, s.d, self.scale, int(bool(chained)),
                   _ptr(self.out), _stream())
         return self.out
+
+    def _check_decode_inputs(self, q_dec, keys, values):
+        """K5 does raw pointer arithmetic with these shapes: bf16, CUDA,
+        contiguous, q_dec [B, L, Hq, n, d], keys == values [B, L, Hkv, T, d]."""
+        import torch
+
+        s = self.shape
+        for name, t in (("q_dec", q_dec), ("keys", keys), ("values", values)):
+            if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous() or t.dim() != 5:
+                raise ValidationError(f"{name}: must be a contiguous 5-D bf16 CUDA tensor")
+        if tuple(q_dec.shape[:3]) != (s.B, s.L, s.Hq) or q_dec.shape[4] != s.d or q_dec.shape[3] < 1:
+            raise ValidationError(f"q_dec: expected [{s.B}, {s.L}, {s.Hq}, n, {s.d}], got {tuple(q_dec.shape)}")
+        if tuple(keys.shape[:3]) != (s.B, s.L, s.Hkv) or keys.shape[4] != s.d:
+            raise ValidationError(f"keys: expected [{s.B}, {s.L}, {s.Hkv}, T, {s.d}], got {tuple(keys.shape)}")
+        if tuple(values.shape) != tuple(keys.shape):
+            raise ValidationError(f"values: shape {tuple(values.shape)} must match keys {tuple(keys.shape)}")
 
     def decode(self, q_dec, keys, values, n_steps=None, graph=True, outputs=None, row0=None, first_step=0):
         """Decode steps first_step .. first_step + n_steps - 1 (default: all of
@@ -308,9 +336,14 @@ class VLCache:
                 if outputs is not None:
                     outputs.append(self.out.clone())
             return self.out
-        key = (q_dec.data_ptr(), keys.data_ptr(), values.data_ptr(), t0, n, row0)
+        self._check_decode_inputs(q_dec, keys, values)
+        # the captured launches bake in pointers AND strides (n_dec, T): key on both
+        key = (q_dec.data_ptr(), tuple(q_dec.shape), keys.data_ptr(), values.data_ptr(), tuple(keys.shape),
+               t0, n, row0)
         g = self._graphs.get(key)
-        if g is None:
+        if g is not None:
+            self._graphs.move_to_end(key)
+        else:
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
@@ -322,6 +355,8 @@ class VLCache:
                 for t in range(t0, t0 + n):
                     self.decode_step(q_dec, keys, values, t, chained=t > t0, row0=row0)
             self._graphs[key] = g
+            while len(self._graphs) > _MAX_GRAPHS:
+                self._graphs.popitem(last=False)
         g.replay()
         return self.out
 
@@ -343,7 +378,8 @@ class VLCache:
                   _ptr(self.col_partial) + slot0 * s.nrb * s.m * 4, _ptr(self.below_head) + slot0 * s.G * 8,
                   0, _ptr(self.exact_ws), self.exact_ws_bytes, _stream())
 
-    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4, dec_chunks=8, dec_early=2):
+    def run_from_host(self, q_win, k_prompt, v_prompt, q_dec, k_dec, v_dec, chunks=4, dec_chunks=8, dec_early=2,
+                      check=True):
         """End-to-end call with pinned HOST inputs (the reference API's setting:
         traces live in host memory): copies Q windows, prompt keys, decode
         queries and the decode steps' K/V rows to the device, compresses --
@@ -355,7 +391,9 @@ class VLCache:
         k/v_prompt [B,L,Hkv,m,d], q_dec [B,L,Hq,n,d], k/v_dec [B,L,Hkv,n,d],
         bf16, pinned.  Returns (kept_counts, out, bytes copied host->device);
         the values pulled zero-copy are zero_copy_bytes(kept_counts) once the
-        stream has synced."""
+        stream has synced.  check=True synchronises at the end and raises like
+        check() (degenerate budget, exact-mode overflow); check=False leaves
+        the copies in flight for the caller to synchronise."""
         import torch
 
         s = self.shape
@@ -372,6 +410,7 @@ class VLCache:
                   torch.empty(self.out.numel(), dtype=torch.float32).pin_memory())
             self._stage = st
             self._copy_stream = torch.cuda.Stream()
+            self._graphs.clear()   # graphs captured on the old staging buffers are stale
         d_qw, d_k, d_qd, d_kn, d_vn, h_counts, h_out = st
         comp, cs = torch.cuda.current_stream(), self._copy_stream
         cs.wait_stream(comp)                  # staging buffers free (previous call done with them)
@@ -426,6 +465,9 @@ class VLCache:
         h_counts.copy_(self.kept_counts, non_blocking=True)
         h_out.copy_(self.out, non_blocking=True)
         copied = sum(t.numel() * 2 for t in (q_win, k_prompt, q_dec, k_dec, v_dec))
+        if check:
+            comp.synchronize()
+            self.check()
         return h_counts, h_out, copied
 
     def zero_copy_bytes(self, host_counts) -> int:
@@ -434,12 +476,36 @@ class VLCache:
         return int(host_counts.sum().item()) * s.Hkv * s.d * 2
 
     # ------------------------------------------------------------ results
+    def exact_stats(self) -> dict:
+        """Exact mode's counters from the last K1 call (synchronises): entries
+        K1 listed for a float64 re-decision, those deferred to an exact row
+        max, rows scanned for it, and `overflow` -- listed entries that found
+        the list full and kept K1's fp32 decision (their below count may then
+        differ from the reference's).  Empty when exact mode is off."""
+        import torch
+
+        if self.exact_ws is None:
+            return {}
+        c = self.exact_ws[:20].view(torch.int32).cpu().tolist()
+        return {"listed": c[1], "deferred": c[0], "rows_scanned": c[3], "overflow": c[2],
+                "capacity": self.exact_capacity}
+
     def check(self):
-        """Synchronise and raise like the reference on a degenerate budget."""
+        """Synchronise and raise like the reference on a degenerate budget
+        (DegenerateSparsityError, reference budget.py:108-109); in exact mode
+        also raise ExactnessError when K1's re-decision list overflowed, so a
+        below count that may differ from the reference's never passes silently."""
         bad = self.status.nonzero()
         if bad.numel():
             raise DegenerateSparsityError(
                 f"every layer is fully sparse; cannot split the budget (batch {bad.flatten().tolist()})")
+        if self.exact_ws is not None:
+            st = self.exact_stats()
+            if st["overflow"]:
+                raise ExactnessError(
+                    f"exact mode: {st['overflow']} of {st['listed']} near-threshold entries found the "
+                    f"re-decision list full (capacity {st['capacity']}) and kept fp32 decisions; "
+                    f"construct VLCache(exact_capacity=...) with room for {st['listed']}")
 
     def kept_sets(self):
         """Host copy: kept[b][l][kv] -> int64 numpy array of ascending indices."""
