@@ -249,12 +249,15 @@ def run_reference_arm(args):
 
 
 # --------------------------------------------------------------------- GPU arm
-def decode_bytes_per_step(kept_counts, step):
+def decode_bytes_per_step(kept_counts, step, hkv=None, hq=None, d=None):
     """Algorithmic HBM bytes of one K5 launch: every cached K
     and V row of every slot read once (k + step + 1 rows), the appended row
-    read + written, Q read, output written."""
+    read + written, Q read, output written.  kept_counts: k_l per (prompt,
+    layer); hkv / hq: the KV / query heads this rank decodes."""
     c = CFG
-    d, hkv, hq = c["head_dim"], c["kv_heads"], c["q_heads"]
+    d = d or c["head_dim"]
+    hkv = hkv or c["kv_heads"]
+    hq = hq or c["q_heads"]
     rows = hkv * (kept_counts + step + 1).sum()
     return (rows * d * 2 * 2 + kept_counts.size * hkv * d * 2 * 2 * 2
             + kept_counts.size * hq * d * (2 + 4))
@@ -338,6 +341,8 @@ def run_gpu_arm(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = CFG
     B, n_dec = args.batch, c["n_out"] - 1
@@ -508,6 +513,136 @@ def run_gpu_arm(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------- sharded configurations
+SHARDED = {
+    # BASELINE.json configs[2]: LLaVA-1.6-34B shapes, batch 4, KV heads sharded across ranks
+    "y34b": dict(layers=60, q_heads=56, kv_heads=8, head_dim=128, prompt_len=10320, tau=64, batch=4,
+                 shard="heads", workload="llava-1.6-34b shapes: L60 Hq56 Hkv8 d128 m10320 (16+5x2048+64) "
+                                           "tau64 alpha0.1 batch4, 99 decode steps"),
+    # BASELINE.json configs[3]: 32 frames x 196 tokens on Mistral-7B shapes, batch 8 sharded by prompt
+    "vid": dict(layers=32, q_heads=32, kv_heads=8, head_dim=128, prompt_len=6352, tau=64, batch=8,
+                shard="batch", workload="video prompt 32 frames x 196 tokens on mistral-7b shapes: L32 Hq32 "
+                                        "Hkv8 d128 m6352 (16+6272+64) tau64 alpha0.1 batch8, 99 decode steps"),
+}
+
+
+def run_sharded_arm(args):
+    """One BASELINE configuration whose global batch is fixed (strong scaling)
+    and sharded over the ranks as SURVEY.md section 8e prescribes:
+      y34b -- KV heads split across ranks (parallel.HeadShard); K1, K3-K5 are
+              local and K2 needs every head's below counts, so each step
+              all-reduces the int64 [B, L, Hq] counts over NCCL inside the
+              timed region (engine.compress -> parallel.exchange_head_counts);
+      vid  -- prompts split across ranks, no collective.
+    Inputs follow the reference generator's recipe, drawn on the device
+    (trace.device_synthetic); timing as the default arm (L2 flushed before each
+    step, CUDA events on the launching stream, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_23317_b200.engine import Shape, VLCache
+    from paper_2410_23317_b200.parallel import HeadShard, shard_batch
+    from paper_2410_23317_b200.trace import GenSpec, device_synthetic
+
+    cf = SHARDED[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L, hq, hkv, d, m, tau, B = (cf[k] for k in ("layers", "q_heads", "kv_heads", "head_dim", "prompt_len", "tau",
+                                                "batch"))
+    g = hq // hkv
+    n_dec = CFG["n_out"] - 1
+    spec = GenSpec(num_layers=L, num_query_heads=hq, num_kv_heads=hkv, head_dim=d, prompt_len=m, post_vision_len=tau,
+                   decode_len=n_dec, seed=0)
+    shard = None
+    if cf["shard"] == "heads":
+        shard = HeadShard(rank, world, hkv, g)
+        (klo, khi), (qlo, qhi) = shard.kv_range, shard.q_range
+        qw, qd, k, v = device_synthetic(spec, B, tau)
+        qw, qd = qw[:, :, qlo:qhi].contiguous(), qd[:, :, qlo:qhi].contiguous()
+        k, v = k[:, :, klo:khi].contiguous(), v[:, :, klo:khi].contiguous()
+        torch.cuda.empty_cache()
+        b_loc, hq_loc, hkv_loc = B, qhi - qlo, khi - klo
+        par = f"kv-head-sharded x{world}: {hkv_loc} KV / {hq_loc} query heads per rank, NCCL int64 all-reduce " \
+              f"of the [B, L, Hq] below counts in every step" if world > 1 else "1 rank (all heads)"
+    else:
+        lo, hi = shard_batch(B, rank, world)
+        qw, qd, k, v = device_synthetic(spec, hi - lo, tau, seed=1000 + lo)
+        b_loc, hq_loc, hkv_loc = hi - lo, hq, hkv
+        par = f"batch-sharded x{world}: prompts [{lo}, {hi}) on rank {rank}, no collective"
+    eng = VLCache(Shape(b_loc, L, hq_loc, hkv_loc, d, m, tau), alpha=CFG["alpha"], p=CFG["p"],
+                  recent_frac=CFG["recent"], decode_steps=n_dec, head_shard=shard)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def step(timers=None):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(st)
+        eng.compress(qw, k, v)
+        e[1].record(st)
+        eng.decode(qd, k, v, graph=True)
+        e[2].record(st)
+        if timers is not None:
+            timers.append(e)
+
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    eng.check()
+    timers = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            step(timers)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    comp = float(np.mean([t[0].elapsed_time(t[1]) for t in timers]))
+    dec = float(np.mean([t[1].elapsed_time(t[2]) for t in timers]))
+    t = torch.tensor([comp + dec, comp, dec], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms, comp_max, dec_max = (float(x) for x in t.tolist())
+    counts = eng.kept_counts.cpu().numpy()
+    by = float(np.mean([decode_bytes_per_step(counts, s_, hkv_loc, hq_loc, d) for s_ in range(n_dec)]))
+    launch_us = dec * 1e3 / n_dec
+    hbm_peak, _, src = peaks()
+    ach = by / (launch_us / 1e6) / 1e9
+    tokens = B * n_dec
+    line = {
+        "metric": METRIC, "value": tokens / (step_ms / 1e3), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: the reference generator's recipe drawn on the device (trace.device_synthetic)",
+        "config": {"workload": cf["workload"], "global_batch": B, "seq_len": m, "parallelism": par,
+                   "l2": "flushed (512 MB write) before every timed step"},
+        "compress_ms_per_prompt": comp_max / B * world if cf["shard"] == "batch" else comp_max / B,
+        "compress_ms_step": comp_max, "decode_ms_99_steps": dec_max,
+        "decode_tokens_per_s": tokens / (dec_max / 1e3),
+        "roofline": {"kernel": "K5 decode_step (rank 0, 99 launches per step, CUDA graph, timed region)",
+                     "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                     "traffic": None, "peak_source": src, "bytes_per_launch": by, "launch_us": launch_us,
+                     "l2_resident": by < 60e6},
+        "gpu_launches": args.steps * (9 + n_dec),
+        "clocks": clk.summary(),
+        "exact_mode": eng.exact_stats(),
+        "kept_tokens_per_layer_mean": float(counts.mean()),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -515,6 +650,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--batch", type=int, default=1, help="prompts per GPU")
+    ap.add_argument("--config", choices=("m7b", *SHARDED), default="m7b",
+                    help="m7b: BASELINE configs[1], one prompt per GPU (weak scaling, the default line); "
+                         "y34b / vid: configs[2] / [3] with their global batch sharded (strong scaling)")
     ap.add_argument("--hbm-batch", type=int, default=8, help="batch of the HBM-resident K5 probe (0: skip)")
     ap.add_argument("--cpu-reps", type=int, default=3, help="runs of the CPU baseline (median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -522,6 +660,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.config != "m7b":
+        run_sharded_arm(args)
     else:
         run_gpu_arm(args)
 

@@ -79,5 +79,10 @@ def exchange_head_counts(local_counts, shard: HeadShard, group=None):
     full = torch.zeros((b, l, shard.num_query_heads), dtype=torch.int64, device=local_counts.device)
     full[:, :, lo:hi] = local_counts
     if shard.world > 1:
-        dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+        if full.is_cuda and dist.get_backend(group) == "gloo":
+            host = full.cpu()     # gloo reduces host memory (the CPU tests' backend)
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+            full.copy_(host)
+        else:
+            dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
     return full

@@ -245,3 +245,74 @@ def test_trace_file_to_run_from_host(tmp_path):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(counts.numpy(), ref.kept_counts.cpu().numpy())
     np.testing.assert_array_equal(out.numpy(), out_ref.cpu().numpy())
+
+
+def test_exact_mode_overflow_raises():
+    """Exact mode with a re-decision list too small for Gaussian logits (many
+    entries near the threshold): check() raises ExactnessError instead of
+    passing fp32 decisions silently; with room for every entry the counts
+    equal the oracle's."""
+    from paper_2410_23317_b200 import ExactnessError
+
+    rng = np.random.default_rng(5)
+    L, HQ, HKV, D, M, TAU = 1, 8, 2, 128, 1500, 64
+    q = bf16(rng.standard_normal((1, L, HQ, TAU, D)) * 2.0)
+    k = bf16(rng.standard_normal((1, L, HKV, M, D)))
+    dq, dk = (torch.from_numpy(x).cuda().to(torch.bfloat16).contiguous() for x in (q, k))
+    small = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), exact_capacity=8)
+    small.compress(dq, dk)
+    with pytest.raises(ExactnessError):
+        small.check()
+    st = small.exact_stats()
+    assert st["overflow"] > 0 and st["listed"] > 8
+    big = VLCache(Shape(1, L, HQ, HKV, D, M, TAU), exact_capacity=st["listed"] + 1024)
+    big.compress(dq, dk)
+    big.check()
+    assert big.exact_stats()["overflow"] == 0
+    ref = O.compression_pass([q[0, 0]], [k[0, 0]], M, HQ // HKV)
+    ref_below = np.array([ref["stats"][(0, h)][3].sum() for h in range(HQ)])
+    np.testing.assert_array_equal(big.below_head.cpu().numpy(), ref_below)
+
+
+def test_decode_rejects_bad_inputs():
+    """K5 does pointer arithmetic with the input shapes: non-contiguous views,
+    wrong dtypes and mismatched K/V raise ValidationError before any launch."""
+    from paper_2410_23317_b200 import ValidationError
+
+    spec = GenSpec(num_layers=1, num_query_heads=4, num_kv_heads=2, head_dim=64, prompt_len=200,
+                   post_vision_len=16, decode_len=3, seed=8)
+    host, dv = make_inputs(spec, 16)
+    eng = VLCache(Shape(1, 1, 4, 2, 64, 200, 16), decode_steps=3)
+    eng.compress(dv["q_win"], dv["keys"], dv["values"])
+    qd, k, v = dv["q_dec"], dv["keys"], dv["values"]
+    with pytest.raises(ValidationError):
+        eng.decode_step(qd.transpose(3, 4).contiguous().transpose(3, 4), k, v, 0)   # non-contiguous
+    with pytest.raises(ValidationError):
+        eng.decode_step(qd.float(), k, v, 0)
+    with pytest.raises(ValidationError):
+        eng.decode_step(qd, k, v[:, :, :, :-1].contiguous(), 0)                    # V shorter than K
+    with pytest.raises(ValidationError):
+        eng.gather(k, v[:, :, :, :-1].contiguous())
+    eng.decode(qd, k, v)   # the valid call still works
+
+
+def test_decode_graph_cache_keys_on_shapes():
+    """Two decode-query tensors that reuse one allocation but differ in their
+    number of decode rows (so in K5's stride) must not share a captured graph."""
+    spec = GenSpec(num_layers=1, num_query_heads=4, num_kv_heads=2, head_dim=64, prompt_len=200,
+                   post_vision_len=16, decode_len=6, seed=10)
+    host, dv = make_inputs(spec, 16)
+    eng = VLCache(Shape(1, 1, 4, 2, 64, 200, 16), decode_steps=3)
+    eng.compress(dv["q_win"], dv["keys"], dv["values"])
+    buf = torch.empty(dv["q_dec"].numel(), dtype=torch.bfloat16, device="cuda")
+    q6 = buf.view(dv["q_dec"].shape)
+    q6.copy_(dv["q_dec"])
+    eng.decode(q6, dv["keys"], dv["values"], n_steps=1)
+    eng.decode(q6, dv["keys"], dv["values"], first_step=1, n_steps=1)        # graph with the 6-row stride
+    q3 = buf[: dv["q_dec"][:, :, :, :3].numel()].view(1, 1, 4, 3, 64)       # same pointer, 3 rows
+    q3.copy_(dv["q_dec"][:, :, :, :3])
+    eng.decode(q3, dv["keys"], dv["values"], first_step=1, n_steps=1)        # must not replay that graph
+    ref = VLCache(Shape(1, 1, 4, 2, 64, 200, 16), decode_steps=3)
+    ref.compress(dv["q_win"], dv["keys"], dv["values"])
+    ref.decode(dv["q_dec"], dv["keys"], dv["values"], graph=False, n_steps=2)
+    np.testing.assert_array_equal(eng.out.cpu().numpy(), ref.out.cpu().numpy())

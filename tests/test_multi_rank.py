@@ -108,3 +108,86 @@ def test_shard_helpers():
 
     with pytest.raises(ValidationError):
         HeadShard(0, 3, 8, 7)
+
+
+# ---------------------------------------------------------------- GPU, 2 ranks on one device
+GL, GHQ, GHKV, GD, GM, GTAU, GN = 3, 56, 8, 128, 1200, 64, 4
+
+
+def _gpu_inputs():
+    from paper_2410_23317_b200.trace import GenSpec, iter_layers, round_to_bf16, synthesize_values
+
+    spec = GenSpec(num_layers=GL, num_query_heads=GHQ, num_kv_heads=GHKV, head_dim=GD, prompt_len=GM,
+                   post_vision_len=GTAU, decode_len=GN, seed=17)
+    qw, qd, ks = [], [], []
+    for k, q in iter_layers(spec, keep_prompt_rows=GTAU):
+        ks.append(round_to_bf16(k))
+        q = round_to_bf16(q)
+        qw.append(q[:, :GTAU])
+        qd.append(q[:, GTAU:])
+    vs = [round_to_bf16(v) for v in synthesize_values(spec)]
+    dev = lambda a: torch.from_numpy(np.stack(a)[None].copy()).cuda().to(torch.bfloat16).contiguous()  # noqa: E731
+    return dev(qw), dev(qd), dev(ks), dev(vs)
+
+
+def _gpu_worker(rank, world, port, q):
+    """One rank of a KV-head-sharded engine (the real VLCache(head_shard=...)
+    path: K1 on its heads, the count exchange, K2-K4, then the decode)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_23317_b200.engine import Shape, VLCache
+
+        torch.cuda.set_device(0)
+        shard = HeadShard(rank=rank, world=world, num_kv_heads=GHKV, group_size=GHQ // GHKV)
+        (klo, khi), (qlo, qhi) = shard.kv_range, shard.q_range
+        qw, qd, k, v = _gpu_inputs()
+        qw, qd = qw[:, :, qlo:qhi].contiguous(), qd[:, :, qlo:qhi].contiguous()
+        k, v = k[:, :, klo:khi].contiguous(), v[:, :, klo:khi].contiguous()
+        eng = VLCache(Shape(1, GL, qhi - qlo, khi - klo, GD, GM, GTAU), decode_steps=GN, head_shard=shard)
+        eng.compress(qw, k, v)
+        eng.decode(qd, k, v)
+        torch.cuda.synchronize()
+        eng.check()
+        q.put((rank, eng.kept_counts.cpu().numpy(), eng.gamma_mean.cpu().numpy(), eng.kept_sets()[0],
+               eng.out.view(GL, qhi - qlo, GD).cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_head_sharded_engine_two_ranks_equals_unsharded():
+    """Two processes on one GPU (gloo, counts staged through the host) drive
+    the real head-sharded engine end to end; budgets, gamma', kept sets and
+    decode outputs equal the unsharded engine's."""
+    from paper_2410_23317_b200.engine import Shape, VLCache
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        r, *rest = q.get(timeout=300)
+        got[r] = rest
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    qw, qd, k, v = _gpu_inputs()
+    full = VLCache(Shape(1, GL, GHQ, GHKV, GD, GM, GTAU), decode_steps=GN)
+    full.compress(qw, k, v)
+    full.decode(qd, k, v)
+    ref_sets = full.kept_sets()[0]
+    ref_out = full.out.view(GL, GHQ, GD).cpu().numpy()
+    for r in range(2):
+        counts, gm, sets, out = got[r]
+        np.testing.assert_array_equal(counts, full.kept_counts.cpu().numpy())
+        np.testing.assert_array_equal(gm, full.gamma_mean.cpu().numpy())
+        shard = HeadShard(rank=r, world=2, num_kv_heads=GHKV, group_size=GHQ // GHKV)
+        (klo, khi), (qlo, qhi) = shard.kv_range, shard.q_range
+        for l in range(GL):
+            for kv in range(khi - klo):
+                np.testing.assert_array_equal(sets[l][kv], ref_sets[l][klo + kv])
+        np.testing.assert_array_equal(out, ref_out[:, qlo:qhi])
