@@ -214,6 +214,30 @@ VLC_API int vlc_attention_rows(const float *q, const float *k, int32_t heads, in
                     int64_t prompt_len, int64_t vision_start, int64_t vision_end, double *mass,
                     void *stream);
 
+/*
+ * The reference kernel seam's float32 contract, for the numpy-in / numpy-out
+ * drop-in of vlcache._kernels (paper_2410_23317_b200._kernels):
+ *
+ * vlc_stats_f32 replaces _core.stats_tiled (reference _core.pyx:210-242):
+ * q f32 [w, d], keys f32 [n, d] (n >= q_base + w), row r sees keys j <= q_base
+ * + r; the reference's arithmetic restated per operation (float64 dots,
+ * float32 logits and exps, float64 sums, `tile`-key blocks in pass 1).
+ * Outputs row_max f32 [w], row_sum f64 [w], col_score f64 [n], below i64 [n],
+ * causal i64 [n] (NULL to skip).  Device pointers.
+ *
+ * vlc_decode_f32 replaces _core.decode_step (reference _core.pyx:245-278):
+ * q f32 [g, d], keys / values f32 [n, d] -> out f32 [g, d]; scratch f32
+ * [g, n] and denom f64 [g] are caller workspace.
+ *
+ * One (layer, head) per call, launch-bound by design; the batched bf16 path is
+ * vlc_score_stats .. vlc_decode_step.
+ */
+VLC_API int vlc_stats_f32(const float *q, const float *keys, int64_t w, int64_t n, int32_t head_dim,
+                    int64_t q_base, double p, int64_t tile, float *row_max, double *row_sum,
+                    double *col_score, int64_t *below, int64_t *causal, void *stream);
+VLC_API int vlc_decode_f32(const float *q, int32_t g, const float *keys, const float *values, int64_t n,
+                    int32_t head_dim, float *scratch, double *denom, float *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,12 +1,16 @@
 """Drop-in for the reference's kernel seam ``vlcache._kernels``.
 
 reference pkg/src/vlcache/_kernels/__init__.py:10-27 exports BACKEND,
-stats_tiled and decode_step with numpy-in/numpy-out semantics.  Here both run
-on the B200 through the C-ABI (K1 with one slot, K5 with one slot); there is
-no CPU fallback -- without the extension or a GPU every call raises
-KernelError.  Inputs are rounded to bf16 on upload (see _device.py).  One
-launch per call makes this seam launch-bound by design; the batched path is
-engine.VLCache.
+stats_tiled and decode_step with numpy-in/numpy-out semantics over float32
+arrays.  Here both run on the B200 through the C-ABI with the reference's
+float32 contract (vlc_stats_f32 / vlc_decode_f32, csrc/seam_f32.cu: float64
+dots, float32 logits and exps, float64 sums, the reference's per-row and
+per-column order), so they can stand in the compiled-extension slot of the
+reference package and its own tests run unmodified over them
+(tests/test_reference_suite.py).  There is no CPU
+fallback -- without the extension or a GPU every call raises KernelError.
+One (layer, head) per call makes this seam launch-bound by design; the
+batched bf16 path is engine.VLCache.
 """
 
 from __future__ import annotations
@@ -30,10 +34,43 @@ def _padded(a: np.ndarray, width: int) -> np.ndarray:
     return out
 
 
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
 def stats_tiled(q, keys, q_base, p, tile):
     """Contract of reference _core.stats_tiled (_core.pyx:210-242):
-    (row_max f32[w], row_sum f64[w], col_score f64[n], below i64[n], causal i64[n]).
-    ``tile`` is the reference's CPU schedule knob; the GPU tiling is fixed."""
+    (row_max f32[w], row_sum f64[w], col_score f64[n], below i64[n], causal i64[n])."""
+    torch = _lib.require_cuda()
+    q = np.asarray(q, dtype=np.float32)
+    keys = np.asarray(keys, dtype=np.float32)
+    if q.ndim != 2 or keys.ndim != 2 or q.shape[1] != keys.shape[1]:
+        raise ValueError("stats_tiled: q [w, d] and keys [n, d] float32 with equal d")
+    w, d = q.shape
+    n = keys.shape[0]
+    if tile < 1:
+        raise ValidationError(f"tile: must be >= 1, got {tile}")
+    if n < q_base + w:
+        raise ValidationError(f"keys: need n >= q_base + w ({q_base + w}), got {n}")
+    qd, kd = _dev(torch, q), _dev(torch, keys)
+    row_max = torch.empty(w, dtype=torch.float32, device="cuda")
+    row_sum = torch.empty(w, dtype=torch.float64, device="cuda")
+    col = torch.empty(n, dtype=torch.float64, device="cuda")
+    below = torch.empty(n, dtype=torch.int64, device="cuda")
+    causal = torch.empty(n, dtype=torch.int64, device="cuda")
+    _lib.call("vlc_stats_f32", qd.data_ptr(), kd.data_ptr(), w, n, d, int(q_base), float(p), int(tile),
+              row_max.data_ptr(), row_sum.data_ptr(), col.data_ptr(), below.data_ptr(), causal.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    return (row_max.cpu().numpy(), row_sum.cpu().numpy(), col.cpu().numpy(), below.cpu().numpy(),
+            causal.cpu().numpy())
+
+
+def stats_tiled_tc(q, keys, q_base, p, tile=128):
+    """K1 -- the batched hot path's tcgen05 kernel with exact mode -- on one
+    slot, with stats_tiled's contract: inputs are rounded to bf16 on upload
+    (the tensor cores' operand type, the "bf16-in" protocol of SURVEY.md
+    section 8).  The parity tests use this to pin K1 against the oracle one
+    (layer, head) at a time."""
     torch = _lib.require_cuda()
     q = np.asarray(q, dtype=np.float32)
     keys = np.asarray(keys, dtype=np.float32)
@@ -92,23 +129,15 @@ def decode_step(q, keys, values):
     n = keys.shape[0]
     if n < 1:
         raise ValidationError("keys: need at least one row")
-    if d > 128:
-        raise ValidationError(f"head_dim: {d} > 128 is not supported")
-    if g > 8:  # the kernel serves up to 8 query heads per KV head
-        return np.concatenate([decode_step(q[i:i + 8], keys, values) for i in range(0, g, 8)])
-    dp = 64 if d <= 64 else 128
-    qd = to_device_bf16(_padded(q, dp))
-    kd = to_device_bf16(_padded(keys, dp))
-    vd = to_device_bf16(_padded(values, dp))
-    # one slot: rows [0, n-1) pre-filled, row n-1 appended by the step itself
-    kc, vc = kd.clone(), vd.clone()
-    cache_off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
-    base_len = torch.tensor([n - 1], dtype=torch.int64, device="cuda")
-    out = torch.empty((g, dp), dtype=torch.float32, device="cuda")
-    _lib.call("vlc_decode_step", qd.data_ptr(), dp, kd[n - 1:].data_ptr(), vd[n - 1:].data_ptr(), dp,
-              kc.data_ptr(), vc.data_ptr(), n, cache_off.data_ptr(), base_len.data_ptr(), 0, 1, 1, 1, g,
-              dp, 1.0 / math.sqrt(d), 0, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
-    return out[:, :d].cpu().numpy()
+    if keys.shape != values.shape or keys.shape[1] != d:
+        raise ValueError("decode_step: keys / values [n, d] float32 matching q [G, d]")
+    qd, kd, vd = _dev(torch, q), _dev(torch, keys), _dev(torch, values)
+    scratch = torch.empty(g * n, dtype=torch.float32, device="cuda")
+    denom = torch.empty(g, dtype=torch.float64, device="cuda")
+    out = torch.empty((g, d), dtype=torch.float32, device="cuda")
+    _lib.call("vlc_decode_f32", qd.data_ptr(), g, kd.data_ptr(), vd.data_ptr(), n, d, scratch.data_ptr(),
+              denom.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    return out.cpu().numpy()
 
 
-__all__ = ["BACKEND", "stats_tiled", "decode_step"]
+__all__ = ["BACKEND", "stats_tiled", "decode_step", "stats_tiled_tc"]

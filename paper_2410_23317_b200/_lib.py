@@ -49,6 +49,8 @@ _SIGNATURES = {
                                    _P, _P, _P, _P]),
     "vlc_attention_rows": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I64, _I64, _I64, _I64, _I64, _P,
                                           _F64, _I64, _I64, _I64, _P, _P]),
+    "vlc_stats_f32": (ctypes.c_int, [_P, _P, _I64, _I64, _I32, _I64, _F64, _I64, _P, _P, _P, _P, _P, _P]),
+    "vlc_decode_f32": (ctypes.c_int, [_P, _I32, _P, _P, _I64, _I32, _P, _P, _P, _P]),
 }
 
 _lib = None

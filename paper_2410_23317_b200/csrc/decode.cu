@@ -65,6 +65,17 @@ VLC_DEV uint32_t swz(int r, int c) {
     return (uint32_t)((c >> 3) * Cfg<D>::kBox + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
+// the per-stage chunk tickets: release / acquire at CTA scope (the issuing
+// thread publishes "stage st now carries chunk c" before arming its barrier)
+VLC_DEV void ticket_store(int* p, int v) {
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(p)), "r"(v) : "memory");
+}
+VLC_DEV int ticket_load(const int* p) {
+    int v;
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(sm100::smem_u32(p)) : "memory");
+    return v;
+}
+
 VLC_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -103,7 +114,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t bar[kStages], empty[kStages];
-    __shared__ volatile int loaded[kStages];   // chunk last issued into each stage
+    __shared__ int loaded[kStages];            // chunk last issued into each stage (ticket)
     __shared__ float part_m[kWarps][8], part_s[kWarps][8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -130,7 +141,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         const int st = c % kStages;
         uint8_t* kdst = smem + st * C::kStage;
         const int y = (int)(seg + (int64_t)c * kChunk);
-        loaded[st] = c;                                          // released by the arrive below
+        ticket_store(&loaded[st], c);
         sm100::mbar_expect_tx(&bar[st], C::kStage);
         for (int kb = 0; kb < C::KB; ++kb) {
             sm100::tma_load_2d(kdst + kb * C::kBox, &kmap, &bar[st], kb * 64, y);
@@ -198,7 +209,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         // A group can run a whole ring ahead of the other: wait until the
         // stage has been re-issued for chunk c before waiting on its phase
         // (a parity wait alone would also accept the stage's previous phase).
-        while (loaded[st] < c) { }
+        while (ticket_load(&loaded[st]) < c) { }
         sm100::mbar_wait(&bar[st], (c / kStages) & 1);
         if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
             wait_prev();                                           // the append is a global write

@@ -102,9 +102,10 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     __shared__ uint64_t full[kStages], empty[kStages], qfull[1], tfull[kAcc], tempty[kAcc];
     __shared__ uint32_t tmem_slot[1];
     __shared__ float2 rowstat[2 * kSets * kM];          // (max, sum) per (set, column half) and row
-    __shared__ __align__(16) float c_mb[kM];            // row max (raw dot) * c1
-    __shared__ __align__(16) float c_is[kM];            // 1 / row sum (0: no row)
-    __shared__ __align__(16) float c_t2[kM];            // threshold on u (-inf: no row)
+    // pass-2 row constants, packed per row pair {mbt_r, mbt_r+1, is_r, is_r+1}:
+    //   mbt = row max * c1 + t2 (u' = l c1 - mbt = log2 e - t2, below <=> u' < 0)
+    //   is  = 2^t2 / row sum   (mass = 2^u' * is = e / S)
+    __shared__ __align__(16) float4 c_pk[kM / 2];
     __shared__ int c_lim[kM];                           // last visible key (-1: no row)
     __shared__ int hcnt[kM];                            // below counts per head of the block
 
@@ -214,7 +215,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int64_t r = r_first + lane_idx;
             const bool row_ok = r < R;
             const int64_t i = row_ok ? r % a.w : 0;
-            const int64_t row_end = row_ok ? imin(a.n, a.q_base + i + 1) : 0;
+            const int row_end32 = row_ok ? (int)imin(a.n, a.q_base + i + 1) : 0;
             float m = -INFINITY, sum = 0.f;
             for (int it = set; it < P1; it += kSets) {
                 const int acc = it % kAcc;
@@ -228,7 +229,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     __syncwarp();
                     if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the tile now
                 }
-                const int valid = (int)imax(0, imin(kSub, row_end - ((int64_t)it * kN + half * 64 + h * kSub)));
+                const int valid = max(0, min(kSub, row_end32 - (it * kN + half * 64 + h * kSub)));
                 const bool full_chunk = __all_sync(kFull, valid == kSub);
                 float cmax;
                 if (full_chunk) {
@@ -243,19 +244,33 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     m = cmax;
                 }
                 const float mb = m * c1;
-                float acc_s[4] = {0.f, 0.f, 0.f, 0.f};   // four chains: ILP for the adds
+                // four add chains (row k -> chain k & 3) as two packed pairs:
+                // FFMA2 for the exponent arguments, FADD2 for the sums
+                float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
+                const float2 c1v = make_float2(c1, c1), nmb = make_float2(-mb, -mb);
                 if (full_chunk) {
 #pragma unroll
+                    for (int k = 0; k < kSub; k += 4) {
+                        const float2 u0 = __ffma2_rn(make_float2(l[k], l[k + 1]), c1v, nmb);
+                        const float2 u1 = __ffma2_rn(make_float2(l[k + 2], l[k + 3]), c1v, nmb);
 #ifdef VLC_K1_NOEX2_TEST
-                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += fmaf(fmaf(l[k], c1, -mb), 0.01f, 1.f);
+                        s01 = __fadd2_rn(s01, __ffma2_rn(u0, make_float2(0.01f, 0.01f), make_float2(1.f, 1.f)));
+                        s23 = __fadd2_rn(s23, __ffma2_rn(u1, make_float2(0.01f, 0.01f), make_float2(1.f, 1.f)));
 #else
-                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += ex2(fmaf(l[k], c1, -mb));
+                        s01 = __fadd2_rn(s01, make_float2(ex2(u0.x), ex2(u0.y)));
+                        s23 = __fadd2_rn(s23, make_float2(ex2(u1.x), ex2(u1.y)));
 #endif
+                    }
                 } else {
 #pragma unroll
-                    for (int k = 0; k < kSub; ++k) acc_s[k & 3] += k < valid ? ex2(fmaf(l[k], c1, -mb)) : 0.f;
+                    for (int k = 0; k < kSub; k += 4) {
+                        const float2 u0 = __ffma2_rn(make_float2(l[k], l[k + 1]), c1v, nmb);
+                        const float2 u1 = __ffma2_rn(make_float2(l[k + 2], l[k + 3]), c1v, nmb);
+                        s01 = __fadd2_rn(s01, make_float2(k < valid ? ex2(u0.x) : 0.f, k + 1 < valid ? ex2(u0.y) : 0.f));
+                        s23 = __fadd2_rn(s23, make_float2(k + 2 < valid ? ex2(u1.x) : 0.f, k + 3 < valid ? ex2(u1.y) : 0.f));
+                    }
                 }
-                sum += (acc_s[0] + acc_s[1]) + (acc_s[2] + acc_s[3]);
+                sum += (s01.x + s01.y) + (s23.x + s23.y);
                 }
             }
             rowstat[(set * 2 + half) * kM + lane_idx] = make_float2(m, sum);
@@ -278,18 +293,18 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     mb = M * c1;
                     rm = M * a.inv_scale;
                 }
+                float* pk = reinterpret_cast<float*>(c_pk) + (lane_idx >> 1) * 4 + (lane_idx & 1);
+                const float t2c = a.t_star * kLog2e;
                 if (row_ok) {
                     a.row_max[(int64_t)s * R + r] = rm;
                     a.row_sum[(int64_t)s * R + r] = S;
-                    c_mb[lane_idx] = mb;
-                    c_is[lane_idx] = 1.f / S;
-                    c_t2[lane_idx] = a.t_star * kLog2e;
+                    pk[0] = mb + t2c;
+                    pk[2] = ex2(t2c) / S;
                     c_lim[lane_idx] = (int)(a.q_base + i);
                 } else {
-                    c_mb[lane_idx] = INFINITY;    // u = -inf: no mass
-                    c_is[lane_idx] = 0.f;
-                    c_t2[lane_idx] = -INFINITY;   // never below
-                    c_lim[lane_idx] = -1;         // sees no key
+                    pk[0] = INFINITY;   // u' = -inf: no mass
+                    pk[2] = 0.f;
+                    c_lim[lane_idx] = -1;         // sees no key (and is never counted)
                 }
             }
             sm100::named_bar_sync(1, kEpiWarps * 32);
@@ -311,73 +326,78 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const int acc = it % kAcc;
             sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
             sm100::tc_fence_after();
-            // exact mode: an entry whose decision u < t2 is within `band` of flipping
+            // exact mode: an entry whose decision u' < 0 is within `band` of flipping
             // (fp32 logits vs the reference's float64 dots) is not counted here but
             // listed for a float64 re-decision.  band = 0: plain decisions.
             const float band = EXACT ? a.band : 0.f;
-            float cs[4] = {0.f, 0.f, 0.f, 0.f};   // mass in four chains (ILP), merged per tile
+            float2 cs01 = make_float2(0.f, 0.f), cs23 = make_float2(0.f, 0.f);   // mass: row k -> chain k & 3
             int cnt = 0;
 #pragma unroll
             for (int h = 0; h < kCh; ++h) {
             const int rh = r0 + h * kSub;                        // first row of this chunk
-            float cf[2] = {0.f, 0.f}, ch[2] = {0.f, 0.f};       // ch - cf: entries inside the band
             tmem_ld(lane_addr + acc * kN + h * kSub, l);
             if (h == kCh - 1) {
                 sm100::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(tempty + acc);
             }
-            // per entry: u = l*c1 - mb_r (log2 of exp(logit - max)), below <=> u < t2_r,
-            // mass += 2^u * (1 / S_r) -- one FFMA, one MUFU, one FFMA; the count
-            // as a float (set + add).  The same operation order in every branch
-            // (chain k & 3 for row k), so identical key columns give bit-identical mass.
-            const float4* mb4 = reinterpret_cast<const float4*>(c_mb + rh);
-            const float4* is4 = reinterpret_cast<const float4*>(c_is + rh);
-            if (all_visible && r_first + rh + kSub - 1 < R) {   // every row real and every key visible
-                const float t2c = a.t_star * kLog2e, t2lo = t2c - band;
+            // per entry: u' = l c1 - mbt_r (log2 of e_r / p-threshold), below <=> u' < 0,
+            // mass += 2^u' * is_r -- packed pairs of rows: one FFMA2, two MUFU, one
+            // FFMA2, two FSET + one FADD2 for the count, one FMNMX3 for the band test.
+            // The same operation order in every branch, so identical key columns
+            // give bit-identical mass (the reference's tie rule needs that).
+            const float4* pk4 = c_pk + (rh >> 1);
+            float minabs = INFINITY;                          // min |u'| over the chunk (band test)
+            float2 cf = make_float2(0.f, 0.f);                // certain-below count
+            const float2 c1v = make_float2(c1, c1);
+            const bool all_rows = r_first + rh + kSub - 1 < R;
+            if (all_visible && all_rows) {   // every row real and every key visible
 #pragma unroll
-                for (int q4 = 0; q4 < kSub / 4; ++q4) {
-                    const float4 mb = mb4[q4], iv = is4[q4];
-                    const float mbv[4] = {mb.x, mb.y, mb.z, mb.w}, ivv[4] = {iv.x, iv.y, iv.z, iv.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float u = fmaf(l[4 * q4 + e], c1, -mbv[e]);
-                        cf[e & 1] += u < t2lo ? 1.f : 0.f;
-                        if (EXACT) ch[e & 1] += u < t2c + band ? 1.f : 0.f;
+                for (int q2 = 0; q2 < kSub / 2; ++q2) {
+                    const float4 c = pk4[q2];
+                    const float2 u = __ffma2_rn(make_float2(l[2 * q2], l[2 * q2 + 1]), c1v, make_float2(-c.x, -c.y));
+                    cf = __fadd2_rn(cf, make_float2(u.x < -band ? 1.f : 0.f, u.y < -band ? 1.f : 0.f));
+                    if (EXACT) minabs = fminf(minabs, fminf(fabsf(u.x), fabsf(u.y)));
 #ifdef VLC_K1_NOEX2_TEST   // timing probe only: is K1 bound by the SFU?
-                        cs[e] = fmaf(fmaf(u, 0.01f, 1.f), ivv[e], cs[e]);
+                    const float2 e = __ffma2_rn(u, make_float2(0.01f, 0.01f), make_float2(1.f, 1.f));
 #else
-                        cs[e] = fmaf(ex2(u), ivv[e], cs[e]);
+                    const float2 e = make_float2(ex2(u.x), ex2(u.y));
 #endif
-                    }
+                    if (q2 & 1) cs23 = __ffma2_rn(e, make_float2(c.z, c.w), cs23);
+                    else cs01 = __ffma2_rn(e, make_float2(c.z, c.w), cs01);
                 }
             } else {
 #pragma unroll
-                for (int k = 0; k < kSub; ++k) {
-                    const bool vis = all_visible || j <= c_lim[rh + k];
-                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
-                    const float t2 = c_t2[rh + k];
-                    cf[k & 1] += (vis && u < t2 - band) ? 1.f : 0.f;
-                    if (EXACT) ch[k & 1] += (vis && u < t2 + band) ? 1.f : 0.f;
-                    cs[k & 3] = vis ? fmaf(ex2(u), c_is[rh + k], cs[k & 3]) : cs[k & 3];
+                for (int q2 = 0; q2 < kSub / 2; ++q2) {
+                    const float4 c = pk4[q2];
+                    const bool v0 = j <= c_lim[rh + 2 * q2], v1 = j <= c_lim[rh + 2 * q2 + 1];
+                    const float2 u = __ffma2_rn(make_float2(l[2 * q2], l[2 * q2 + 1]), c1v, make_float2(-c.x, -c.y));
+                    cf = __fadd2_rn(cf, make_float2((v0 && u.x < -band) ? 1.f : 0.f, (v1 && u.y < -band) ? 1.f : 0.f));
+                    if (EXACT) minabs = fminf(minabs, fminf(v0 ? fabsf(u.x) : INFINITY, v1 ? fabsf(u.y) : INFINITY));
+                    const float2 e = make_float2(v0 ? ex2(u.x) : 0.f, v1 ? ex2(u.y) : 0.f);
+                    if (q2 & 1) cs23 = __ffma2_rn(e, make_float2(c.z, c.w), cs23);
+                    else cs01 = __ffma2_rn(e, make_float2(c.z, c.w), cs01);
                 }
             }
-            const float cntf = cf[0] + cf[1], cnth = ch[0] + ch[1];
-            if (EXACT && __any_sync(kFull, cnth != cntf)) {
-                // reserve this thread's entries with one atomic, then write them
-                const int nf = (int)(cnth - cntf);
+            const float cntf = cf.x + cf.y;
+            if (EXACT && __any_sync(kFull, minabs < band)) {
+                // list this thread's in-band entries (one atomic reserves them all)
+                int nf = 0;
+#pragma unroll
+                for (int k = 0; k < kSub; ++k) {
+                    const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
+                    nf += (j < a.n && j <= c_lim[rh + k] && fabsf(u) < band) ? 1 : 0;
+                }
                 int at = nf ? atomicAdd(a.fix_counts + 1, nf) : 0;
 #pragma unroll
                 for (int k = 0; k < kSub; ++k) {   // static indices: l stays in registers
-                    const bool vis = j < a.n && (all_visible || j <= c_lim[rh + k]);
-                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
-                    const float t2 = c_t2[rh + k];
-                    if (nf && vis && u >= t2 - band && u < t2 + band) {
+                    const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
+                    if (nf && j < a.n && j <= c_lim[rh + k] && fabsf(u) < band) {
                         if (at < a.cap) {
                             a.flag[at] = make_int4(s, (int)(r_first + rh + k), j, 1);
-                        } else {   // list full: keep the fp32 decision
+                        } else {   // list full: keep the fp32 decision (reported as overflow)
                             atomicAdd(a.fix_counts + 2, 1);
-                            cnt += u < t2 ? 1 : 0;
+                            cnt += u < 0.f ? 1 : 0;
                         }
                         ++at;
                     }
@@ -387,14 +407,13 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             if (!one_head) {
 #pragma unroll
                 for (int k = 0; k < kSub; ++k) {
-                    const bool vis = all_visible || j <= c_lim[rh + k];
-                    const float u = fmaf(l[k], c1, -c_mb[rh + k]);
-                    const int tot = __reduce_add_sync(kFull, (vis && u < c_t2[rh + k] - band) ? 1 : 0);
+                    const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
+                    const int tot = __reduce_add_sync(kFull, (j <= c_lim[rh + k] && u < -band) ? 1 : 0);
                     if (lane == 0 && tot) atomicAdd(hcnt + (int)((r_first + rh + k) / a.w - head0), tot);
                 }
             }
             }
-            if (j < a.n) colp[j] = (cs[0] + cs[1]) + (cs[2] + cs[3]);
+            if (j < a.n) colp[j] = (cs01.x + cs01.y) + (cs23.x + cs23.y);
             if (a.below_col && cnt && j < a.n) atomicAdd(a.below_col + (int64_t)s * a.n + j, cnt);
             // per-head totals (warp reduce, one shared atomic per warp)
             if (one_head) {   // (mixed-head halves were counted row by row above)

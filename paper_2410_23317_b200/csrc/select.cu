@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
                 }
                 const unsigned excl = incl - tot;
                 const long long want = s_want;
+                __syncwarp();   // every lane has read s_want before the selecting lane rewrites it
                 const bool mine = (long long)excl < want && want <= (long long)incl;
                 if (mine) {
                     long long cum = excl;

@@ -342,4 +342,31 @@ int vlc_decode_step(const void* q, int64_t q_stride, const void* k_new, const vo
     return cuda_status(vlc::launch_decode(a, (cudaStream_t)stream), "decode_step");
 }
 
+int vlc_stats_f32(const float* q, const float* keys, int64_t w, int64_t n, int32_t head_dim, int64_t q_base,
+                  double p, int64_t tile, float* row_max, double* row_sum, double* col_score, int64_t* below,
+                  int64_t* causal, void* stream) {
+    if (!q || !keys || !row_max || !row_sum || !col_score || !below) return fail(VLC_EINVAL, "stats_f32: null pointer");
+    if (w < 1 || n < 1 || head_dim < 1 || q_base < 0 || tile < 1)
+        return fail(VLC_EINVAL, "stats_f32: need w, n, head_dim, tile >= 1 and q_base >= 0");
+    if (n < q_base + w)
+        return fail(VLC_EINVAL, "stats_f32: n %lld < q_base + w %lld", (long long)n, (long long)(q_base + w));
+    if (!(p >= 0.0)) return fail(VLC_EINVAL, "p: must be >= 0, got %g", p);
+    vlc::SeamStatsArgs a{};
+    a.q = q; a.k = keys; a.w = w; a.n = n; a.q_base = q_base; a.tile = tile; a.d = head_dim;
+    a.inv = 1.0 / std::sqrt((double)head_dim);   // reference _core.pyx:222
+    a.p = p; a.row_max = row_max; a.row_sum = row_sum; a.col_score = col_score; a.below = below; a.causal = causal;
+    return cuda_status(vlc::launch_seam_stats(a, (cudaStream_t)stream), "stats_f32");
+}
+
+int vlc_decode_f32(const float* q, int32_t g, const float* keys, const float* values, int64_t n, int32_t head_dim,
+                   float* scratch, double* denom, float* out, void* stream) {
+    if (!q || !keys || !values || !scratch || !denom || !out) return fail(VLC_EINVAL, "decode_f32: null pointer");
+    if (g < 1 || g > 65535 || n < 1 || head_dim < 1) return fail(VLC_EINVAL, "decode_f32: need g in [1, 65535], n, head_dim >= 1");
+    vlc::SeamDecodeArgs a{};
+    a.q = q; a.k = keys; a.v = values; a.n = n; a.g = g; a.d = head_dim;
+    a.inv = (float)(1.0 / std::sqrt((double)head_dim));   // reference _core.pyx:257
+    a.scratch = scratch; a.denom = denom; a.out = out;
+    return cuda_status(vlc::launch_seam_decode(a, (cudaStream_t)stream), "decode_f32");
+}
+
 }  // extern "C"

@@ -165,4 +165,33 @@ struct RowsArgs {
 int64_t attention_rows_smem(int64_t d, int64_t span);
 cudaError_t launch_attention_rows(const RowsArgs& a, cudaStream_t st);
 
+// The reference kernel seam's float32 contract (seam_f32.cu).
+struct SeamStatsArgs {
+    const float* q;            // f32 [w, d]
+    const float* k;            // f32 [n, d]
+    int64_t w, n, q_base, tile;
+    int d;
+    double inv;                // 1 / sqrt(d), float64
+    double p;
+    float* row_max;            // f32 [w]
+    double* row_sum;           // f64 [w]
+    double* col_score;         // f64 [n]
+    int64_t* below;            // i64 [n]
+    int64_t* causal;           // i64 [n] or null
+};
+cudaError_t launch_seam_stats(const SeamStatsArgs& a, cudaStream_t st);
+
+struct SeamDecodeArgs {
+    const float* q;            // f32 [g, d]
+    const float* k;            // f32 [n, d]
+    const float* v;            // f32 [n, d]
+    int64_t n;
+    int g, d;
+    float inv;                 // float32(1 / sqrt(d))
+    float* scratch;            // f32 [g, n]
+    double* denom;             // f64 [g]
+    float* out;                // f32 [g, d]
+};
+cudaError_t launch_seam_decode(const SeamDecodeArgs& a, cudaStream_t st);
+
 }  // namespace vlc

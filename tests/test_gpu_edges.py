@@ -89,7 +89,7 @@ def test_stats_window_smaller_than_tau_matches_oracle():
 def test_stats_tiny_and_ragged(w, n, qb):
     rng = np.random.default_rng(w * 7 + n)
     q, k = bf16(rng.standard_normal((w, 64))), bf16(rng.standard_normal((n, 64)))
-    got = _kernels.stats_tiled(q, k, qb, 0.01, 128)
+    got = _kernels.stats_tiled_tc(q, k, qb, 0.01, 128)
     ref = O.stats_tiled(q, k, qb, 0.01, 128)
     np.testing.assert_allclose(got[0], ref[0], rtol=1e-6)
     np.testing.assert_allclose(got[2], ref[2], rtol=1e-5, atol=1e-12)

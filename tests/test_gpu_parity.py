@@ -45,7 +45,7 @@ def test_score_stats_matches_oracle(seed, w, n, d, qb):
     rng = np.random.default_rng(seed)
     q = bf16(rng.standard_normal((w, d)) * (2.0 if seed >= 8 else 1.0))
     k = bf16(rng.standard_normal((n, d)))
-    got = _kernels.stats_tiled(q, k, qb, 0.01, 128)
+    got = _kernels.stats_tiled_tc(q, k, qb, 0.01, 128)
     ref = O.stats_tiled(q, k, qb, 0.01, 128)
     np.testing.assert_allclose(got[0], ref[0], rtol=1e-6, atol=0)
     np.testing.assert_allclose(got[1], ref[1], rtol=1e-5, atol=0)
@@ -61,10 +61,10 @@ def test_p_extremes():
     logit ties, decided from float64 dots by K1's exact mode."""
     rng = np.random.default_rng(7)
     q, k = bf16(rng.standard_normal((64, 32))), bf16(rng.standard_normal((64, 32)))
-    got = _kernels.stats_tiled(q, k, 0, 1e-300, 32)
+    got = _kernels.stats_tiled_tc(q, k, 0, 1e-300, 32)
     ref = O.stats_tiled(q, k, 0, 1e-300, 32)
     np.testing.assert_array_equal(got[3], ref[3])
-    got = _kernels.stats_tiled(q, k, 0, 1.0, 32)
+    got = _kernels.stats_tiled_tc(q, k, 0, 1.0, 32)
     ref = O.stats_tiled(q, k, 0, 1.0, 32)
     np.testing.assert_array_equal(got[3], ref[3])
 
@@ -316,3 +316,31 @@ def test_fixed_budgets_through_compress_cache(golden):
         ref = [[O.evict(scores[l, kv], int(alloc.kept_counts[l])) for kv in range(scores.shape[1])]
                for l in range(L)]
         check_kept_sets(got, ref, scores, alloc.kept_counts)
+
+
+@pytest.mark.parametrize("seed,w,n,d,qb,tile", [
+    (0, 96, 96, 32, 0, 32), (1, 96, 96, 32, 0, 17), (2, 40, 128, 64, 88, 33), (3, 4, 256, 32, 252, 64),
+    (4, 1, 64, 16, 63, 4096), (5, 200, 200, 48, 0, 128), (6, 64, 2960, 128, 2896, 256),
+])
+def test_seam_f32_matches_reference_arithmetic(seed, w, n, d, qb, tile):
+    """The kernel seam (vlcache._kernels drop-in) on float32 inputs -- the
+    reference's own test_kernels.py CASES: the device restates _core.pyx's
+    arithmetic per operation, so the statistics equal the C restatement (itself
+    bit-identical to the compiled reference) up to glibc expf's rare 1-ulp
+    departures from correct rounding (the device rounds exp(double) once)."""
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((w, d)).astype(np.float32)
+    k = rng.standard_normal((n, d)).astype(np.float32)
+    got = _kernels.stats_tiled(q, k, qb, 0.01, tile)
+    ref = O.stats_tiled(q, k, qb, 0.01, tile)
+    np.testing.assert_array_equal(got[0], ref[0])                       # row max: same float32 logits
+    np.testing.assert_allclose(got[1], ref[1], rtol=1e-7, atol=0)
+    np.testing.assert_allclose(got[2], ref[2], rtol=1e-7, atol=1e-300)
+    np.testing.assert_array_equal(got[3], ref[3])
+    np.testing.assert_array_equal(got[4], ref[4])
+    for g_, n_ in ((1, 33), (4, 512), (7, 3000)):
+        qq = rng.standard_normal((g_, d)).astype(np.float32)
+        kk = rng.standard_normal((n_, d)).astype(np.float32)
+        vv = rng.standard_normal((n_, d)).astype(np.float32)
+        np.testing.assert_allclose(_kernels.decode_step(qq, kk, vv), O.decode_step(qq, kk, vv), rtol=1e-6,
+                                   atol=1e-7)
