@@ -34,6 +34,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_want;
     __shared__ unsigned long long s_min, s_max;
+    __shared__ int s_small;                        // bucket small enough for the warp finish
+    __shared__ unsigned long long s_cand[32];      // its keys
+    __shared__ int s_ncand;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = blockIdx.x;
@@ -48,23 +51,53 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
     //    or the caller's float64 scores when scores_in is given (evict API)
     unsigned long long kmin = ~0ull, kmax = 0ull;
     const double group = (double)a.G;
-    for (int64_t j = tid; j < n; j += kThreads) {
-        double sc;
+    // U keys per thread at a time with all their partial loads issued before
+    // any is consumed (4 x U loads in flight instead of one dependent load at a
+    // time); the partials still add in row-block order (fixed, position-free)
+    constexpr int U = 4;
+    for (int64_t j0 = tid; j0 < n; j0 += U * kThreads) {
+        double sc[U];
         if (a.scores_in) {
-            sc = a.scores_in[(int64_t)s * n + j];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t j = j0 + (int64_t)u * kThreads;
+                sc[u] = j < n ? a.scores_in[(int64_t)s * n + j] : 0.0;
+            }
         } else {
-            double acc = 0.0;
-            const float* cp = a.col_partial + (int64_t)s * a.nrb * n + j;
-            for (int rb = 0; rb < a.nrb; ++rb) acc = __dadd_rn(acc, (double)cp[(int64_t)rb * n]);
-            sc = __ddiv_rn(acc, group);
-            if (a.scores) a.scores[(int64_t)s * n + j] = sc;
+            const float* cp = a.col_partial + (int64_t)s * a.nrb * n;
+            double acc[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = 0.0;
+            for (int rb0 = 0; rb0 < a.nrb; rb0 += 4) {
+                float x[4][U];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int64_t j = j0 + (int64_t)u * kThreads;
+                        x[r][u] = (rb0 + r < a.nrb && j < n) ? cp[(int64_t)(rb0 + r) * n + j] : 0.f;
+                    }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (rb0 + r < a.nrb) acc[u] = __dadd_rn(acc[u], (double)x[r][u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) sc[u] = __ddiv_rn(acc[u], group);
         }
-        const unsigned long long key = order_key(sc);
-        keys[j] = key;
-        if (j < ncand) { kmin = min(kmin, key); kmax = max(kmax, key); }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = j0 + (int64_t)u * kThreads;
+            if (j >= n) continue;
+            if (!a.scores_in && a.scores) a.scores[(int64_t)s * n + j] = sc[u];
+            const unsigned long long key = order_key(sc[u]);
+            keys[j] = key;
+            if (j < ncand) { kmin = min(kmin, key); kmax = max(kmax, key); }
+        }
     }
     __syncthreads();
-    if (tid == 0) { s_min = ~0ull; s_max = 0ull; s_prefix = 0ull; s_mask = 0ull; s_want = nk; }
+    if (tid == 0) { s_min = ~0ull; s_max = 0ull; s_prefix = 0ull; s_mask = 0ull; s_want = nk; s_small = 0; s_ncand = 0; }
     __syncthreads();
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -121,15 +154,45 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
                 if (mine) {
                     long long cum = excl;
                     int sel = 0;
+                    unsigned cnt = 0;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
-                        if (cum + c[q] >= want) { sel = 255 - 8 * lane - q; break; }
+                        if (cum + c[q] >= want) { sel = 255 - 8 * lane - q; cnt = c[q]; break; }
                         cum += c[q];
                     }
                     s_want = want - cum;
                     s_prefix = prefix | ((unsigned long long)sel << shift);
                     s_mask = mask | (255ull << shift);
+                    // a bucket of <= 32 keys is finished by one warp (no more passes)
+                    s_small = (pass > 0 && cnt <= 32) ? 1 : 0;
                 }
+            }
+            __syncthreads();
+            if (s_small) break;
+        }
+        if (s_small) {
+            // gather the bucket's keys, sort them descending in one warp (bitonic
+            // over the lanes), the want-th is T
+            const unsigned long long prefix = s_prefix, mask = s_mask;
+            for (int64_t j = tid; j < ncand; j += kThreads)
+                if ((keys[j] & mask) == prefix) s_cand[atomicAdd(&s_ncand, 1)] = keys[j];
+            __syncthreads();
+            if (warp == 0) {
+                unsigned long long x = lane < s_ncand ? s_cand[lane] : 0ull;
+#pragma unroll
+                for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+                    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                        const unsigned long long y = __shfl_xor_sync(kFull, x, stride);
+                        const bool desc = (lane & size) == 0;          // descending blocks
+                        const bool lower = (lane & stride) == 0;
+                        x = (lower == desc) ? max(x, y) : min(x, y);
+                    }
+                }
+                const long long want = s_want;                         // 1 <= want <= bucket size
+                const unsigned long long t = __shfl_sync(kFull, x, (int)(want - 1));
+                const long long above = __popc(__ballot_sync(kFull, lane < s_ncand && x > t));
+                if (lane == 0) { s_prefix = t; s_want = want - above; }
             }
             __syncthreads();
         }

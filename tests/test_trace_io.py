@@ -50,3 +50,43 @@ def test_error_modes(tmp_path):
     (tmp_path / "ver").write_bytes(raw[:4] + (2).to_bytes(4, "little") + raw[8:])
     with pytest.raises(errors.TraceFormatError):
         read_trace(tmp_path / "ver")
+
+
+def _cli_kwargs(args):
+    """The reference CLI flags of a golden run as compress_outputs arguments."""
+    kw, i = {}, 0
+    names = {"--policy": ("policy", str), "--budget": ("budget", str), "--sliding-window": ("sliding_window", int),
+             "--alpha": ("alpha", float), "--recent-frac": ("recent_frac", float),
+             "--stats-window": ("stats_window", int)}
+    while i < len(args):
+        key, typ = names[args[i]]
+        kw[key] = typ(args[i + 1])
+        i += 2
+    return kw
+
+
+@pytest.mark.gpu
+def test_compress_outputs_equal_reference_cli_files(tmp_path):
+    """allocation.json / kept_sets.json byte-identical to the reference CLI's
+    `compress` (cli.py:195-203) for several policy x budget choices
+    (tests/golden/cli_golden.json, tests/golden/make_cli_golden.py)."""
+    import json as _json
+    import os as _os
+
+    from paper_2410_23317_b200.outputs import write_compress_outputs
+    from paper_2410_23317_b200.trace import AttentionTrace, GenSpec, generate_trace, round_to_bf16
+
+    with open(_os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "golden", "cli_golden.json")) as f:
+        golden = _json.load(f)
+    traces = {}
+    for name, spec in golden["specs"].items():
+        tr, _ = generate_trace(GenSpec(**spec))
+        traces[name] = AttentionTrace(header=tr.header, layout=tr.layout,
+                                      queries=[round_to_bf16(x) for x in tr.queries],
+                                      keys=[round_to_bf16(x) for x in tr.keys])
+    for i, run in enumerate(golden["runs"]):
+        out = tmp_path / f"run{i}"
+        stdout = write_compress_outputs(out, traces[run["trace"]], **_cli_kwargs(run["args"]))
+        assert (out / "allocation.json").read_text() == run["allocation.json"], run["args"]
+        assert (out / "kept_sets.json").read_text() == run["kept_sets.json"], run["args"]
+        assert _json.dumps(stdout) == run["stdout"].strip(), run["args"]
