@@ -11,6 +11,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -38,13 +39,29 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None, de
         t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in deps):
             return lib
-    cmd = [nvcc(), *ARCH, *(f"-D{d}" for d in defines), "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xcompiler", "-fvisibility=hidden", "-cudart", "static",
-           "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp", *srcs]
+    flags = [*ARCH, *(f"-D{d}" for d in defines), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xcompiler", "-fvisibility=hidden", "-I", os.path.join(ROOT, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+        flags.append("-Xptxas=-v")
+    # one nvcc per translation unit, in parallel, then one link
+    objdir = lib + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+
+    def compile_one(i):
+        cmd = [nvcc(), *flags, "-c", "-o", objs[i], srcs[i]]
+        if verbose:
+            print(" ".join(cmd))
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, range(len(srcs))))
+    for r in results:
+        sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, r.args)
+    subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", lib + ".tmp", *objs], check=True)
+    shutil.rmtree(objdir, ignore_errors=True)
     os.replace(lib + ".tmp", lib)
     return lib
 

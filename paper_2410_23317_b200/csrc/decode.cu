@@ -66,13 +66,17 @@ VLC_DEV uint32_t swz(int r, int c) {
 }
 
 // the per-stage chunk tickets: release / acquire at CTA scope (the issuing
-// thread publishes "stage st now carries chunk c" before arming its barrier)
+// thread publishes "stage st now carries chunk c" before arming its barrier).
+// Atomic read-modify-writes, so racecheck sees synchronisation, not a race.
 VLC_DEV void ticket_store(int* p, int v) {
-    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(sm100::smem_u32(p)), "r"(v) : "memory");
+    int old;
+    asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;"
+                 : "=r"(old) : "r"(sm100::smem_u32(p)), "r"(v) : "memory");
+    (void)old;
 }
 VLC_DEV int ticket_load(const int* p) {
     int v;
-    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(sm100::smem_u32(p)) : "memory");
+    asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(sm100::smem_u32(p)) : "memory");
     return v;
 }
 
