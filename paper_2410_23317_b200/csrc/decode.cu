@@ -21,7 +21,9 @@
 // partials merge once at the end.  Under programmatic dependent launch only
 // the chunk holding the previous step's append (and the global writes) wait
 // for the previous step: everything else is loaded and computed while it
-// drains.  A stage is refilled as soon as the four
+// drains.  Each stage has two full barriers used alternately, so a group that
+// runs a ring ahead of the other never mistakes a stage's previous use for its
+// chunk.  A stage is refilled as soon as the four
 // warps that consumed it arrive on its "empty" barrier.  The chunk holding row
 // k + step takes it from k_new / v_new (patched into the swizzled tile) and
 // also appends it to the cache for later steps.
@@ -65,21 +67,6 @@ VLC_DEV uint32_t swz(int r, int c) {
     return (uint32_t)((c >> 3) * Cfg<D>::kBox + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
-// the per-stage chunk tickets: release / acquire at CTA scope (the issuing
-// thread publishes "stage st now carries chunk c" before arming its barrier).
-// Atomic read-modify-writes, so racecheck sees synchronisation, not a race.
-VLC_DEV void ticket_store(int* p, int v) {
-    int old;
-    asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;"
-                 : "=r"(old) : "r"(sm100::smem_u32(p)), "r"(v) : "memory");
-    (void)old;
-}
-VLC_DEV int ticket_load(const int* p) {
-    int v;
-    asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(sm100::smem_u32(p)) : "memory");
-    return v;
-}
-
 VLC_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
@@ -117,8 +104,11 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     using C = Cfg<D>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar[kStages], empty[kStages];
-    __shared__ int loaded[kStages];            // chunk last issued into each stage (ticket)
+    // two full barriers per stage, alternating by the stage's use (chunk c is
+    // use c / kStages): a group running a ring ahead of the refills waits on
+    // the other barrier of the pair, whose pending phase cannot be mistaken
+    // for its chunk's (a parity wait alone would accept the previous use)
+    __shared__ uint64_t bar[kStages][2], empty[kStages];
     __shared__ float part_m[kWarps][8], part_s[kWarps][8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -132,9 +122,9 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
 
     if (tid == 0) {
         for (int i = 0; i < kStages; ++i) {
-            sm100::mbar_init(&bar[i], 1);
+            sm100::mbar_init(&bar[i][0], 1);
+            sm100::mbar_init(&bar[i][1], 1);
             sm100::mbar_init(&empty[i], kGroupWarps);
-            loaded[i] = -1;
         }
         sm100::fence_barrier_init();
         sm100::tma_prefetch(&kmap);
@@ -145,11 +135,11 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         const int st = c % kStages;
         uint8_t* kdst = smem + st * C::kStage;
         const int y = (int)(seg + (int64_t)c * kChunk);
-        ticket_store(&loaded[st], c);
-        sm100::mbar_expect_tx(&bar[st], C::kStage);
+        uint64_t* fb = &bar[st][(c / kStages) & 1];
+        sm100::mbar_expect_tx(fb, C::kStage);
         for (int kb = 0; kb < C::KB; ++kb) {
-            sm100::tma_load_2d(kdst + kb * C::kBox, &kmap, &bar[st], kb * 64, y);
-            sm100::tma_load_2d(kdst + C::kTile + kb * C::kBox, &vmap, &bar[st], kb * 64, y);
+            sm100::tma_load_2d(kdst + kb * C::kBox, &kmap, fb, kb * 64, y);
+            sm100::tma_load_2d(kdst + C::kTile + kb * C::kBox, &vmap, fb, kb * 64, y);
         }
     };
     // Programmatic dependent launch.  When the caller guarantees that the
@@ -210,11 +200,8 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         const int64_t j0 = (int64_t)c * kChunk;
         uint8_t* ks = smem + st * C::kStage;
         uint8_t* vs = ks + C::kTile;
-        // A group can run a whole ring ahead of the other: wait until the
-        // stage has been re-issued for chunk c before waiting on its phase
-        // (a parity wait alone would also accept the stage's previous phase).
-        while (ticket_load(&loaded[st]) < c) { }
-        sm100::mbar_wait(&bar[st], (c / kStages) & 1);
+        // chunk c is use c / kStages of its stage: wait on that use's barrier
+        sm100::mbar_wait(&bar[st][(c / kStages) & 1], (c / (2 * kStages)) & 1);
         if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
             wait_prev();                                           // the append is a global write
             const int r = (int)(new_row - j0);

@@ -63,6 +63,12 @@ SM100_DEV void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
                  : "memory");
 }
 
+// bring `bytes` (multiple of 16) of global memory into L2 (no barrier)
+SM100_DEV void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+                 : "memory");
+}
+
 // 1-D bulk copy global -> shared (bytes % 16 == 0), completion on `bar`
 SM100_DEV void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
