@@ -403,8 +403,14 @@ def run_gpu_arm(args):
     counts = eng.kept_counts.view(B, c["layers"]).cpu().numpy()
     eng.score_stats(d_qw, d_k); eng.allocate(); eng.select(); eng.gather(d_k, d_v)
     per = []
+    # cold flush: the 512 MB write, then a 512 MB read, so L2 holds clean lines
+    # only (a write alone leaves ~126 MB of dirty lines whose write-back would
+    # be charged to the launch: +4 us, tools/k5_cold.py)
+    rd = torch.ones(L2_FLUSH_BYTES // 8, dtype=torch.int64, device="cuda")
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     for s_ in range(n_dec):
         flush.zero_()
+        sink.add_(rd.sum())
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         eng.decode_step(d_qd, d_k, d_v, s_)
@@ -431,7 +437,8 @@ def run_gpu_arm(args):
                                 "launches of a step, so this fraction is of L2-fed bytes, not HBM",
                 "cold": {"launch_us": float(np.mean(k5_cold_ms)) * 1e3, "achieved": k5_cold_gbs,
                          "frac": k5_cold_gbs / hbm_peak,
-                         "how": "each launch alone after a 512 MB L2 flush (all bytes from HBM)"}}
+                         "how": "each launch alone after a 512 MB L2 flush (write, then read: clean "
+                                "lines only) -- all bytes from HBM"}}
         if args.hbm_batch > 1 and world == 1:
             roof["hbm"] = k5_hbm_probe(args.hbm_batch, (d_qw, d_qd, d_k, d_v), shape, hbm_peak, flush, torch)
     else:
