@@ -43,6 +43,10 @@ constexpr int kN = 128;          // keys per tile (UMMA N)
 #define VLC_K1_MINB 1
 #endif
 constexpr int kStages = VLC_K1_STAGES;   // K tile ring
+#ifndef VLC_K1_L2AHEAD
+#define VLC_K1_L2AHEAD 0
+#endif
+constexpr int kL2Ahead = VLC_K1_L2AHEAD;   // key tiles prefetched into L2 beyond the ring
 constexpr int kSub = VLC_K1_SUB;         // TMEM columns an epilogue thread holds at a time (16 / 32)
 #ifndef VLC_K1_SETS
 #define VLC_K1_SETS 2
@@ -90,6 +94,24 @@ VLC_DEV void tmem_ld(uint32_t taddr, float (&v)[N]) {
     if constexpr (N == 32) sm100::tmem_ld32(taddr, v);
     else sm100::tmem_ld16(taddr, v);
 }
+// split issue / wait: the next chunk's TMEM load runs under this chunk's math
+template <int N>
+VLC_DEV void tmem_issue(uint32_t taddr, uint32_t (&r)[N]) {
+    if constexpr (N == 32) sm100::tmem_ld32_issue(taddr, r);
+    else sm100::tmem_ld16_issue(taddr, r);
+}
+template <int N>
+VLC_DEV void tmem_wait(uint32_t (&r)[N]) {
+    if constexpr (N == 32) sm100::tmem_ld32_wait(r);
+    else sm100::tmem_ld16_wait(r);
+}
+#ifndef VLC_K1_PIPE
+#define VLC_K1_PIPE 0
+#endif
+constexpr bool kPipe = VLC_K1_PIPE;   // software-pipelined TMEM loads in the epilogue
+#ifndef VLC_K1_PROBE
+#define VLC_K1_PROBE 0   // timing probes (wrong results), bits: 1 = no epilogue math, 2 = no MMA, 4 = no TMA after the first ring
+#endif
 
 template <int D, bool EXACT>
 __global__ void __launch_bounds__(kThreads, VLC_K1_MINB)
@@ -155,10 +177,20 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             sm100::mbar_expect_tx(qfull, LY::kQBytes);
             for (int kb = 0; kb < LY::KB; ++kb)
                 sm100::tma_load_2d(smem + kb * LY::kQRegion, &qmap, qfull, kb * 64, (int)(s * R + r_first));
+            // pull the first pass's key tiles into L2 ahead of their loads (the
+            // ring holds only kStages tiles; the rest of the L2 latency is hidden)
+            auto l2_prefetch = [&](int t) {
+                for (int kb = 0; kb < LY::KB; ++kb)
+                    sm100::tma_prefetch_2d(&kmap, kb * 64, (int)(s * a.T + (int64_t)t * kN));
+            };
+            const int pf_first = P1 > 0 ? P1 : iters;   // tiles of the first pass over the keys
+            for (int t = kStages; t < kStages + kL2Ahead && t < pf_first; ++t) l2_prefetch(t);
             for (int it = 0; it < iters; ++it) {
                 const int st = it % kStages;
                 const uint32_t ph = (it / kStages) & 1;
                 const int t = it < P1 ? it : tlo + (it - P1);
+                if ((VLC_K1_PROBE & 4) && it >= kStages) break;
+                if (kL2Ahead > 0 && it + kStages + kL2Ahead < pf_first) l2_prefetch(it + kStages + kL2Ahead);
                 sm100::mbar_wait(empty + st, ph ^ 1);
                 sm100::mbar_expect_tx(full + st, LY::kKBytes);
                 uint8_t* kdst = smem + LY::kQBytes + st * LY::kKBytes;
@@ -179,7 +211,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 const int acc = it % kAcc;
                 const uint32_t aph = (it / kAcc) & 1;
                 sm100::mbar_wait(tempty + acc, aph ^ 1);
-                sm100::mbar_wait(full + st, ph);
+                if (!((VLC_K1_PROBE & 4) && it >= kStages)) sm100::mbar_wait(full + st, ph);
                 sm100::tc_fence_after();
                 const uint32_t k_addr = sm100::smem_u32(smem + LY::kQBytes + st * LY::kKBytes);
                 const bool rows_on_lanes = it < P1;
@@ -189,6 +221,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     for (int kk = 0; kk < 4; ++kk) {   // 4 x 16 elements = one 128 B swizzle row
                         const uint64_t qd = sm100::sdesc_k_sw128(q_addr + kb * LY::kQRegion + kk * 32);
                         const uint64_t kd = sm100::sdesc_k_sw128(k_addr + kb * LY::kKRegion + kk * 32);
+                        if (!(VLC_K1_PROBE & 2))   // timing probe: no MMA
                         sm100::mma_bf16(tmem + acc * kN, rows_on_lanes ? qd : kd, rows_on_lanes ? kd : qd, idesc,
                                         (kb | kk) != 0);
                     }
@@ -221,14 +254,24 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                 const int acc = it % kAcc;
                 sm100::mbar_wait(tfull + acc, (it / kAcc) & 1);
                 sm100::tc_fence_after();
+                uint32_t rbuf[2][kSub];
+                if (kPipe) tmem_issue(lane_addr + acc * kN, rbuf[0]);
 #pragma unroll
                 for (int h = 0; h < kCh; ++h) {
-                tmem_ld(lane_addr + acc * kN + h * kSub, l);
+                if (kPipe) {
+                    tmem_wait(rbuf[h & 1]);
+                    if (h + 1 < kCh) tmem_issue(lane_addr + acc * kN + (h + 1) * kSub, rbuf[(h + 1) & 1]);
+#pragma unroll
+                    for (int i = 0; i < kSub; ++i) l[i] = __uint_as_float(rbuf[h & 1][i]);
+                } else {
+                    tmem_ld(lane_addr + acc * kN + h * kSub, l);
+                }
                 if (h == kCh - 1) {
                     sm100::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) sm100::mbar_arrive(tempty + acc);   // registers hold the tile now
                 }
+                if (VLC_K1_PROBE & 1) { sum += l[0]; continue; }   // timing probe: no epilogue math
                 const int valid = max(0, min(kSub, row_end32 - (it * kN + half * 64 + h * kSub)));
                 const bool full_chunk = __all_sync(kFull, valid == kSub);
                 float cmax;
@@ -332,15 +375,25 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
             const float band = EXACT ? a.band : 0.f;
             float2 cs01 = make_float2(0.f, 0.f), cs23 = make_float2(0.f, 0.f);   // mass: row k -> chain k & 3
             int cnt = 0;
+            uint32_t rbuf[2][kSub];
+            if (kPipe) tmem_issue(lane_addr + acc * kN, rbuf[0]);
 #pragma unroll
             for (int h = 0; h < kCh; ++h) {
             const int rh = r0 + h * kSub;                        // first row of this chunk
-            tmem_ld(lane_addr + acc * kN + h * kSub, l);
+            if (kPipe) {
+                tmem_wait(rbuf[h & 1]);
+                if (h + 1 < kCh) tmem_issue(lane_addr + acc * kN + (h + 1) * kSub, rbuf[(h + 1) & 1]);
+#pragma unroll
+                for (int i = 0; i < kSub; ++i) l[i] = __uint_as_float(rbuf[h & 1][i]);
+            } else {
+                tmem_ld(lane_addr + acc * kN + h * kSub, l);
+            }
             if (h == kCh - 1) {
                 sm100::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) sm100::mbar_arrive(tempty + acc);
             }
+            if (VLC_K1_PROBE & 1) { cs01.x += l[0]; continue; }   // timing probe: no epilogue math
             // per entry: u' = l c1 - mbt_r (log2 of e_r / p-threshold), below <=> u' < 0,
             // mass += 2^u' * is_r -- packed pairs of rows: one FFMA2, two MUFU, one
             // FFMA2, two FSET + one FADD2 for the count, one FMNMX3 for the band test.
