@@ -71,10 +71,25 @@ VLC_API int64_t vlc_score_partials(int64_t rows);
  * and row_max equal the reference's for bf16-representable inputs.
  * exact_ws: 256-byte aligned, >= vlc_score_exact_bytes(slots, group, window,
  * E) bytes for room for E listed entries (E >= slots*G*w is ample; beyond
- * capacity the fp32 decision is kept).
+ * capacity the fp32 decision is kept).  After the call (stream-ordered) its
+ * first 32 bytes hold the status words, int32 unless noted:
+ *   [0] entries deferred to an exact row max   [1] entries listed by K1
+ *   [2] OVERFLOW: listed entries that kept the fp32 decision (list full; the
+ *       below counts may then differ from the reference's)
+ *   [3] rows whose exact max was recomputed    [4] keys the row scan listed
+ *   [5] f32: largest observed |tensor-core logit - exact logit| (listed entries)
+ *   [6] f32: largest observed |fp32 row max - exact row max| (recomputed rows)
+ * [5] and [6] check the margins exact mode relies on (VLC_EXACT_BAND_LOGIT,
+ * VLC_EXACT_ROWMAX_ERR): callers treat [5] + [6] > VLC_EXACT_BAND_LOGIT / 8
+ * or [6] > VLC_EXACT_ROWMAX_ERR / 2 like an overflow.
  * Requires n_keys >= q_base + window, head_dim in {64, 128} (zero-pad smaller
  * dims and pass their scale), 16-byte aligned q_win / keys.
  */
+/* exact mode's fixed margins (logit units): K1 decides itself every entry
+ * farther than BAND from the threshold; the fix-up decides against K1's fp32
+ * row max when farther than ROWMAX_ERR */
+#define VLC_EXACT_BAND_LOGIT (1.0 / 512.0 / 1.4426950408889634)
+#define VLC_EXACT_ROWMAX_ERR (1.0 / 512.0 / 1.4426950408889634 / 16.0)
 VLC_API int64_t vlc_score_exact_bytes(int32_t slots, int32_t group, int64_t window, int64_t entries);
 VLC_API int vlc_score_stats(const void *q_win, const void *keys, int32_t slots, int32_t group,
                     int32_t head_dim, int64_t key_rows, int64_t n_keys, int64_t window,

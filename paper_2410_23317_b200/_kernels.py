@@ -21,7 +21,10 @@ import numpy as np
 
 from . import _lib
 from ._device import causal_per_column, to_device_bf16
-from .errors import ValidationError
+from .errors import ExactnessError, ValidationError
+
+EXACT_BAND_LOGIT = 1.0 / 512.0 / 1.4426950408889634   # include/vlc.h VLC_EXACT_BAND_LOGIT
+EXACT_ROWMAX_ERR = EXACT_BAND_LOGIT / 16.0             # include/vlc.h VLC_EXACT_ROWMAX_ERR
 
 BACKEND = "b200"
 
@@ -108,8 +111,13 @@ def stats_tiled_tc(q, keys, q_base, p, tile=128):
                   1.0 / math.sqrt(d), row_max.data_ptr(), row_sum.data_ptr(), col.data_ptr(),
                   below_head.data_ptr(), below_col.data_ptr(), ws.data_ptr(), ws_bytes,
                   torch.cuda.current_stream().cuda_stream)
-        counters = ws[:20].view(torch.int32).cpu().tolist()   # [deferred, listed, overflow, ...]
+        status = ws[:32].cpu()
+        counters = status.view(torch.int32).tolist()   # [deferred, listed, overflow, ...] (include/vlc.h)
         if counters[2] == 0:
+            errs = status.view(torch.float32).tolist()
+            if errs[5] + errs[6] > EXACT_BAND_LOGIT / 8 or errs[6] > EXACT_ROWMAX_ERR / 2:
+                raise ExactnessError(f"exact mode: observed tensor-core logit error {errs[5]:.3g} / row-max "
+                                     f"error {errs[6]:.3g} approach the exact-mode margins")
             break
         cap = max(2 * cap, counters[1] + 1024)
         del ws

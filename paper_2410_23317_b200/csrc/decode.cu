@@ -50,6 +50,12 @@ constexpr int kChunk = 16 * kGroupWarps;        // rows per ring stage
 #define VLC_DEC_STAGES 3
 #endif
 constexpr int kStages = VLC_DEC_STAGES;
+#ifndef VLC_DEC_SCHAINS
+#define VLC_DEC_SCHAINS 2   // accumulator chains of S = K Q^T (1 or 2)
+#endif
+#ifndef VLC_DEC_PROBE
+#define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring
+#endif
 
 template <int D>
 struct Cfg {
@@ -201,7 +207,8 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         uint8_t* ks = smem + st * C::kStage;
         uint8_t* vs = ks + C::kTile;
         // chunk c is use c / kStages of its stage: wait on that use's barrier
-        sm100::mbar_wait(&bar[st][(c / kStages) & 1], (c / (2 * kStages)) & 1);
+        if (!((VLC_DEC_PROBE & 2) && c >= kStages))
+            sm100::mbar_wait(&bar[st][(c / kStages) & 1], (c / (2 * kStages)) & 1);
         if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
             wait_prev();                                           // the append is a global write
             const int r = (int)(new_row - j0);
@@ -217,17 +224,42 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             }
             sm100::named_bar_sync(1 + grp, kGroupWarps * 32);
         }
+        if (VLC_DEC_PROBE & 1) {   // timing probe: no math
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&empty[st]);
+            if (wig == 0 && lane == 0 && c + kStages < nchunks) {
+                sm100::mbar_wait(&empty[st], (c / kStages) & 1);
+                if (c + kStages == pend) wait_prev();
+                issue(c + kStages);
+            }
+            continue;
+        }
         // ---- S^T = K Q^T for this warp's 16 keys
         const int kr = wig * 16;                               // first key of the warp
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t kbase = sm100::smem_u32(ks);
         const int arow = kr + (lane & 7) + ((lane >> 3) & 1) * 8;   // ldmatrix row of this lane
+#if VLC_DEC_SCHAINS == 2
+        // two independent accumulator chains over the k-steps (half the HMMA latency chain)
+        float sacc2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < D / 16; kk += 2) {
+            uint32_t af[4], ag[4];
+            ldsm_x4(kbase + swz<D>(arow, kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
+            ldsm_x4(kbase + swz<D>(arow, (kk + 1) * 2 + (lane >> 4)), ag[0], ag[1], ag[2], ag[3]);
+            mma16(sacc, af, qb[kk][0], qb[kk][1]);
+            mma16(sacc2, ag, qb[kk + 1][0], qb[kk + 1][1]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sacc[i] += sacc2[i];
+#else
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
             uint32_t af[4];
             ldsm_x4(kbase + swz<D>(arow, kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
             mma16(sacc, af, qb[kk][0], qb[kk][1]);
         }
+#endif
         // ---- online softmax per head over the warp's keys: thread holds keys
         //      kr+row (c0, c1) and kr+row+8 (c2, c3) for heads 2q (c0, c2), 2q+1 (c1, c3)
         const int64_t ja = j0 + kr + row, jb = ja + 8;
@@ -274,7 +306,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         // stage consumed by this group's warps -> refill it (the group leader)
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&empty[st]);
-        if (wig == 0 && lane == 0 && c + kStages < nchunks) {
+        if (wig == 0 && lane == 0 && c + kStages < nchunks && !(VLC_DEC_PROBE & 2)) {
             sm100::mbar_wait(&empty[st], (c / kStages) & 1);
             if (c + kStages == pend) wait_prev();             // holds the previous step's append
             issue(c + kStages);

@@ -69,9 +69,12 @@ __global__ void fix_flags(ScoreArgs a) {
     const int n = min(a.fix_counts[1], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 e = a.flag[i];
+        const int4 f = a.flag[i];
+        const int4 e = make_int4(f.x, f.y, f.z, 1);
         const int64_t rr = (int64_t)e.x * R + e.y;
         const float l = exact_logit<D>(a, e.x, e.y, e.z);
+        // the tensor-core logit's observed error (the margins' runtime check)
+        atomicMax(reinterpret_cast<unsigned*>(a.fix_counts + 5), __float_as_uint(fabsf(l - __int_as_float(f.w) * a.inv_scale)));
         const float x = l - a.row_max[rr];
         if (x < a.t_star - a.err_max) {
             add_below(a, e);
@@ -202,7 +205,9 @@ __global__ void fix_deferred(ScoreArgs a) {
     }
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < a.fix_counts[3]; q += stride) {
         const int64_t rr = a.rows[q];
-        a.row_max[rr] = funkey(a.rmax_key[rr]);
+        const float exact = funkey(a.rmax_key[rr]);
+        atomicMax(reinterpret_cast<unsigned*>(a.fix_counts + 6), __float_as_uint(fabsf(exact - a.row_max[rr])));
+        a.row_max[rr] = exact;
     }
 }
 

@@ -447,7 +447,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
                     if (nf && j < a.n && j <= c_lim[rh + k] && fabsf(u) < band) {
                         if (at < a.cap) {
-                            a.flag[at] = make_int4(s, (int)(r_first + rh + k), j, 1);
+                            a.flag[at] = make_int4(s, (int)(r_first + rh + k), j, __float_as_int(l[k]));   // .w: the fp32 dot
                         } else {   // list full: keep the fp32 decision (reported as overflow)
                             atomicAdd(a.fix_counts + 2, 1);
                             cnt += u < 0.f ? 1 : 0;

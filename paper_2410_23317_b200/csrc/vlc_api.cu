@@ -149,8 +149,9 @@ static int score_stats_impl(const void* q_win, const void* keys, int32_t slots, 
         a.cand = reinterpret_cast<int4*>(ws + 256 + 2 * rk);
         a.flag = a.cand + cap;
         a.cap = cap;
-        a.band = 1.0f / 512.0f;   // log2 units: ~100x the fp32-accumulation error of a d <= 128 logit
-        a.err_max = a.band / 1.4426950408889634f / 16.0f;  // logit units (~10x the fp32 row-max error)
+        // margins (include/vlc.h); the fix-ups record the errors they observe against them
+        a.band = (float)(VLC_EXACT_BAND_LOGIT * 1.4426950408889634);   // log2 units: 2^-9
+        a.err_max = (float)VLC_EXACT_ROWMAX_ERR;                         // logit units
     }
     return cuda_status(vlc::launch_score_stats(a, (cudaStream_t)stream), "score_stats");
 }

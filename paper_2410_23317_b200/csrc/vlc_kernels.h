@@ -41,7 +41,7 @@ struct ScoreArgs {
     // exact mode (fix != nullptr): entries whose below-threshold decision is
     // within `band` (log2 units) of flipping, and the near-max entries that
     // decide the row max, are listed and re-decided in float64 afterwards
-    int* fix_counts;                   // device [n_defer, n_flag, overflow, n_rows] (zeroed by the launcher)
+    int* fix_counts;                   // device [n_defer, n_flag, overflow, n_rows, n_scan, max logit err (f32), max row-max err (f32), -] (zeroed by the launcher)
     unsigned* rmax_key;                // [slots*R] 1 = row listed, then key of its exact f32 max (0 = none)
     int* rows;                         // [slots*R] rows whose exact max is needed
     int4* cand;                        // [cap] (slot, row, key, mult) entries waiting for an exact row max

@@ -25,6 +25,7 @@ from collections import OrderedDict
 from dataclasses import dataclass
 
 from . import _lib
+from ._kernels import EXACT_BAND_LOGIT, EXACT_ROWMAX_ERR
 from .errors import DegenerateSparsityError, ExactnessError, ValidationError
 
 _ROW_BLOCK = 128  # K1 rows per CTA; col_partial has 2 partials (64-row halves) per block
@@ -486,9 +487,12 @@ class VLCache:
 
         if self.exact_ws is None:
             return {}
-        c = self.exact_ws[:20].view(torch.int32).cpu().tolist()
+        w = self.exact_ws[:32].cpu()
+        c = w.view(torch.int32).tolist()
+        f = w.view(torch.float32).tolist()
         return {"listed": c[1], "deferred": c[0], "rows_scanned": c[3], "overflow": c[2],
-                "capacity": self.exact_capacity}
+                "capacity": self.exact_capacity, "max_logit_err": f[5], "max_rowmax_err": f[6],
+                "margin_ok": bool(f[5] + f[6] <= EXACT_BAND_LOGIT / 8 and f[6] <= EXACT_ROWMAX_ERR / 2)}
 
     def check(self):
         """Synchronise and raise like the reference on a degenerate budget
@@ -506,6 +510,11 @@ class VLCache:
                     f"exact mode: {st['overflow']} of {st['listed']} near-threshold entries found the "
                     f"re-decision list full (capacity {st['capacity']}) and kept fp32 decisions; "
                     f"construct VLCache(exact_capacity=...) with room for {st['listed']}")
+            if not st["margin_ok"]:
+                raise ExactnessError(
+                    f"exact mode: observed tensor-core logit error {st['max_logit_err']:.3g} / row-max error "
+                    f"{st['max_rowmax_err']:.3g} approach the margins K1 decides with ({EXACT_BAND_LOGIT:.3g} / "
+                    f"{EXACT_ROWMAX_ERR:.3g} logit units); below counts may differ from the reference's")
 
     def kept_sets(self):
         """Host copy: kept[b][l][kv] -> int64 numpy array of ascending indices."""

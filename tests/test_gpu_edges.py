@@ -274,6 +274,30 @@ def test_exact_mode_overflow_raises():
     np.testing.assert_array_equal(big.below_head.cpu().numpy(), ref_below)
 
 
+def test_exact_mode_margin_check():
+    """Exact mode's fixed margins are verified at run time: the fix-ups record
+    the largest tensor-core logit / row-max errors they observe.  On Gaussian
+    logits (many listed entries) those stay far inside the margins; a status
+    word past a margin makes check() raise ExactnessError."""
+    from paper_2410_23317_b200 import ExactnessError
+    from paper_2410_23317_b200.engine import EXACT_BAND_LOGIT
+
+    rng = np.random.default_rng(6)
+    L, HQ, HKV, D, M, TAU = 1, 8, 2, 128, 1500, 64
+    q = bf16(rng.standard_normal((1, L, HQ, TAU, D)) * 2.0)
+    k = bf16(rng.standard_normal((1, L, HKV, M, D)))
+    dq, dk = (torch.from_numpy(x).cuda().to(torch.bfloat16).contiguous() for x in (q, k))
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, TAU))
+    eng.compress(dq, dk)
+    eng.check()
+    st = eng.exact_stats()
+    assert st["listed"] > 100 and st["margin_ok"]
+    assert 0.0 < st["max_logit_err"] < EXACT_BAND_LOGIT / 50, st
+    eng.exact_ws[20:24].view(torch.float32).fill_(EXACT_BAND_LOGIT / 4)   # [5]: a logit error past the margin
+    with pytest.raises(ExactnessError):
+        eng.check()
+
+
 def test_decode_rejects_bad_inputs():
     """K5 does pointer arithmetic with the input shapes: non-contiguous views,
     wrong dtypes and mismatched K/V raise ValidationError before any launch."""
