@@ -26,7 +26,11 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-__global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
+// RK > 0: n <= RK * kThreads, each thread keeps its RK keys (j = tid + u *
+// kThreads) in registers for the radix passes and issues all their partial
+// loads at once; RK == 0: any n, keys re-read from shared / global memory.
+template <int RK>
+__global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
     pdl_wait_then_release();
     extern __shared__ unsigned long long keys_smem[];
     __shared__ unsigned int hist[256];
@@ -54,7 +58,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
     // U keys per thread at a time with all their partial loads issued before
     // any is consumed (4 x U loads in flight instead of one dependent load at a
     // time); the partials still add in row-block order (fixed, position-free)
-    constexpr int U = 4;
+    constexpr int U = RK > 0 ? RK : 4;
+    unsigned long long kreg[RK > 0 ? RK : 1];
     for (int64_t j0 = tid; j0 < n; j0 += U * kThreads) {
         double sc[U];
         if (a.scores_in) {
@@ -89,6 +94,7 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t j = j0 + (int64_t)u * kThreads;
+            if (RK > 0) kreg[RK > 0 ? u : 0] = order_key(sc[u]);
             if (j >= n) continue;
             if (!a.scores_in && a.scores) a.scores[(int64_t)s * n + j] = sc[u];
             const unsigned long long key = order_key(sc[u]);
@@ -127,12 +133,25 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
             for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
             __syncthreads();
             const unsigned long long prefix = s_prefix, mask = s_mask;
-            for (int64_t j0 = 0; j0 < ncand; j0 += kThreads) {
-                const int64_t j = j0 + tid;
-                const bool in = j < ncand && ((keys[j] & mask) == prefix);
-                const unsigned dgt = in ? (unsigned)((keys[j] >> shift) & 255u) : 256u;
-                const unsigned peers = __match_any_sync(kFull, dgt);
-                if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
+            if (RK > 0) {
+#pragma unroll
+                for (int u = 0; u < (RK > 0 ? RK : 1); ++u) {
+                    const int64_t j = tid + (int64_t)u * kThreads;
+                    const bool in = j < ncand && ((kreg[u] & mask) == prefix);
+                    if (!__any_sync(kFull, in)) continue;   // warp-uniform
+                    const unsigned dgt = in ? (unsigned)((kreg[u] >> shift) & 255u) : 256u;
+                    const unsigned peers = __match_any_sync(kFull, dgt);
+                    if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
+                }
+            } else {
+                for (int64_t j0 = 0; j0 < ncand; j0 += kThreads) {
+                    const int64_t j = j0 + tid;
+                    const bool in = j < ncand && ((keys[j] & mask) == prefix);
+                    if (!__any_sync(kFull, in)) continue;   // warp-uniform
+                    const unsigned dgt = in ? (unsigned)((keys[j] >> shift) & 255u) : 256u;
+                    const unsigned peers = __match_any_sync(kFull, dgt);
+                    if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
+                }
             }
             __syncthreads();
             if (warp == 0) {
@@ -174,8 +193,16 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
             // gather the bucket's keys, sort them descending in one warp (bitonic
             // over the lanes), the want-th is T
             const unsigned long long prefix = s_prefix, mask = s_mask;
-            for (int64_t j = tid; j < ncand; j += kThreads)
-                if ((keys[j] & mask) == prefix) s_cand[atomicAdd(&s_ncand, 1)] = keys[j];
+            if (RK > 0) {
+#pragma unroll
+                for (int u = 0; u < (RK > 0 ? RK : 1); ++u) {
+                    const int64_t j = tid + (int64_t)u * kThreads;
+                    if (j < ncand && (kreg[u] & mask) == prefix) s_cand[atomicAdd(&s_ncand, 1)] = kreg[u];
+                }
+            } else {
+                for (int64_t j = tid; j < ncand; j += kThreads)
+                    if ((keys[j] & mask) == prefix) s_cand[atomicAdd(&s_ncand, 1)] = keys[j];
+            }
             __syncthreads();
             if (warp == 0) {
                 unsigned long long x = lane < s_ncand ? s_cand[lane] : 0ull;
@@ -241,8 +268,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(SelectArgs a) {
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st) {
     if (a.n > kSmemKeysMax && !a.key_scratch) return cudaErrorInvalidValue;  // needs global scratch
     const size_t sm = a.n <= kSmemKeysMax ? sizeof(unsigned long long) * (size_t)a.n : 0;
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemKeysMax * 8));
-    return launch_pdl(select_kernel, dim3(a.slots), dim3(kThreads), sm, st, a);
+    if (a.n <= 6 * kThreads) return launch_pdl(select_kernel<6>, dim3(a.slots), dim3(kThreads), sm, st, a);
+    cudaFuncSetAttribute(select_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kSmemKeysMax * 8));
+    return launch_pdl(select_kernel<0>, dim3(a.slots), dim3(kThreads), sm, st, a);
 }
 
 }  // namespace vlc

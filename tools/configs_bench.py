@@ -1,7 +1,9 @@
-"""The path at every BASELINE.json configuration that fits one B200, with
-random bf16 inputs generated on the device (the reference generator needs
-~20 GB of fp32 host memory at Y34B; parity at these sizes is covered by the
-size-independent checks below and at smaller sizes by tests/):
+"""The path at every BASELINE.json configuration that fits one B200, on the
+reference generator's recipe drawn on the device (trace.device_synthetic; the
+host generator needs ~20 GB of fp32 at Y34B -- oracle parity at these shapes
+is tests/test_gpu_configs.py), K1 in exact mode, the L2 flushed (512 MB
+write + read) before every timed call, SM clocks and throttle reasons sampled
+by NVML during the timed calls:
 
   M7B    LLaVA-1.6-Mistral-7B shapes, batch 1            (the bench.py workload)
   Y34B   LLaVA-1.6-34B shapes (L60, Hq56, Hkv8), batch 4 x 5 images x 2K visual
@@ -18,7 +20,7 @@ indices, and decode step 0 of 8 sampled slots against a float64 torch reference.
 """
 import argparse
 
-EXACT = False
+EXACT = True
 import json
 import math
 import os
@@ -28,7 +30,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 from paper_2410_23317_b200.engine import Shape, VLCache  # noqa: E402
+from paper_2410_23317_b200.trace import GenSpec, device_synthetic  # noqa: E402
 
 N_DEC = 99
 CONFIGS = {
@@ -39,26 +43,33 @@ CONFIGS = {
 }
 
 
+FLUSH = None
+CLOCKS = None
+
+
 def timed(fn, reps=5):
+    global FLUSH
+    if FLUSH is None:
+        FLUSH = (torch.empty(512 << 20, dtype=torch.uint8, device="cuda"),
+                 torch.ones(512 << 20, dtype=torch.uint8, device="cuda"), torch.zeros(1, device="cuda"))
     ts = []
     for _ in range(reps):
+        FLUSH[0].zero_()
+        FLUSH[2].add_(FLUSH[1][::4096].float().sum())   # then a read: no dirty lines left in L2
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
-        torch.cuda.synchronize()
+        with CLOCKS:
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     return float(np.median(ts[1:]))
 
 
 def inputs(c, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    B, L, Hq, Hkv, d, m, tau = (c[k] for k in ("B", "L", "Hq", "Hkv", "d", "m", "tau"))
-    bf = torch.bfloat16
-    qw = (torch.randn((B, L, Hq, tau, d), device="cuda", generator=g) * 2).to(bf)
-    k = torch.randn((B, L, Hkv, m + N_DEC, d), device="cuda", generator=g).to(bf)
-    v = torch.randn((B, L, Hkv, m + N_DEC, d), device="cuda", generator=g).to(bf)
-    qd = torch.randn((B, L, Hq, N_DEC, d), device="cuda", generator=g).to(bf)
+    spec = GenSpec(num_layers=c["L"], num_query_heads=c["Hq"], num_kv_heads=c["Hkv"], head_dim=c["d"],
+                   prompt_len=c["m"], post_vision_len=c["tau"], decode_len=N_DEC, seed=seed)
+    qw, qd, k, v = device_synthetic(spec, c["B"], c["tau"])
     return qw, k, v, qd
 
 
@@ -96,9 +107,8 @@ def run(name, c):
     flops = 2 * c["d"] * c["Hq"] * causal * c["L"] * c["B"]
     for alpha in c["alphas"]:
         full = alpha == "full"
-        # random Gaussian logits put a large share of entries near the p threshold,
-        # where exact mode re-decides each in float64 (bench.py measures exact
-        # mode on the generator's inputs); here the plain fp32 decisions unless --exact
+        global CLOCKS
+        CLOCKS = bench.ClockSampler(torch.cuda.current_device())
         eng = VLCache(shape, alpha=1.0 if full else alpha, decode_steps=N_DEC, exact=EXACT)
         if full:
             zeros = torch.zeros((c["B"], c["L"]), dtype=torch.float64, device="cuda")
@@ -120,7 +130,8 @@ def run(name, c):
              "m": c["m"], "kept_mean": float(counts.mean()), "compress_ms_per_prompt": t_comp / c["B"],
              "k1_ms": t_k1, "k1_tflops": flops / (t_k1 / 1e3) / 1e12, "decode_us_per_step": t_dec * 1e3 / N_DEC,
              "k5_gbs": by / N_DEC / (t_dec / 1e3 / N_DEC) / 1e9, "tok_s": c["B"] * N_DEC / ((t_comp + t_dec) / 1e3),
-             "decode_tok_s": c["B"] * N_DEC / (t_dec / 1e3), "decode_rel_err_vs_f64": worst}
+             "decode_tok_s": c["B"] * N_DEC / (t_dec / 1e3), "decode_rel_err_vs_f64": worst,
+             "exact_mode": eng.exact_stats() if EXACT else None, "clocks": CLOCKS.summary()}
         print(json.dumps(r), flush=True)
         res.append(r)
         del eng
@@ -136,16 +147,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=",".join(CONFIGS))
     ap.add_argument("--out", default=None)
-    ap.add_argument("--exact", action="store_true", help="K1 exact mode (slow on random inputs)")
+    ap.add_argument("--fp32", action="store_true", help="K1 with plain fp32 decisions (exact mode off)")
     args = ap.parse_args()
     global EXACT
-    EXACT = args.exact
+    EXACT = not args.fp32
     allres = []
     for name in args.only.split(","):
         allres += run(name, CONFIGS[name])
     if args.out:
         with open(args.out, "w") as f:
-            json.dump({"device": torch.cuda.get_device_name(), "inputs": "device randn (q x2), bf16",
+            json.dump({"device": torch.cuda.get_device_name(),
+                       "inputs": "reference generator recipe drawn on the device (trace.device_synthetic), bf16",
+                       "l2": "flushed (512 MB write + read) before every timed call",
                        "k1_decisions": "exact mode" if EXACT else "fp32 (exact mode off: random logits)",
                        "results": allres}, f, indent=1)
 

@@ -4,15 +4,16 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/launch_floor tools/launch_floor.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e_)); return -1.f; } } while (0)
 
 __global__ void k_plain(float* out) {
-    extern __shared__ float sm[];
+    __shared__ float sm[1];
     if (threadIdx.x == 0) sm[0] = out[blockIdx.x];
     __syncthreads();
     if (threadIdx.x == 0) out[blockIdx.x] = sm[0] + 1.f;
 }
 __global__ void k_pdl(float* out) {
-    extern __shared__ float sm[];
+    __shared__ float sm[1];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) sm[0] = out[blockIdx.x];
@@ -22,11 +23,11 @@ __global__ void k_pdl(float* out) {
 
 static float run(bool pdl, int grid, int smem, float* buf) {
     cudaStream_t st;
-    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    auto fn = pdl ? k_pdl : k_plain;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    void (*fn)(float*) = pdl ? k_pdl : k_plain;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaGraph_t g;
-    cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < 99; ++i) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -38,9 +39,9 @@ static float run(bool pdl, int grid, int smem, float* buf) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
-        cudaLaunchKernelEx(&cfg, fn, buf);
+        CK(cudaLaunchKernelEx(&cfg, fn, buf));
     }
-    cudaStreamEndCapture(st, &g);
+    CK(cudaStreamEndCapture(st, &g));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { printf("capture: %s\n", cudaGetErrorString(e)); return -1.f; }
     cudaGraphExec_t ge;
@@ -51,10 +52,10 @@ static float run(bool pdl, int grid, int smem, float* buf) {
     cudaEventCreate(&b);
     float best = 1e9;
     for (int rep = 0; rep < 10; ++rep) {
-        cudaEventRecord(a, st);
-        cudaGraphLaunch(ge, st);
-        cudaEventRecord(b, st);
-        cudaEventSynchronize(b);
+        CK(cudaEventRecord(a, st));
+        CK(cudaGraphLaunch(ge, st));
+        CK(cudaEventRecord(b, st));
+        CK(cudaEventSynchronize(b));
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         if (rep >= 2 && ms < best) best = ms;
