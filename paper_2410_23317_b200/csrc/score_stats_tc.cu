@@ -110,7 +110,7 @@ VLC_DEV void tmem_wait(uint32_t (&r)[N]) {
 #endif
 constexpr bool kPipe = VLC_K1_PIPE;   // software-pipelined TMEM loads in the epilogue
 #ifndef VLC_K1_PROBE
-#define VLC_K1_PROBE 0   // timing probes (wrong results), bits: 1 = no epilogue math, 2 = no MMA, 4 = no TMA after the first ring
+#define VLC_K1_PROBE 0   // timing probes (wrong results), bits: 1 = no epilogue math, 2 = no MMA, 4 = no TMA after the first ring, 8 = one TMEM load per tile
 #endif
 
 template <int D, bool EXACT>
@@ -264,7 +264,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                     for (int i = 0; i < kSub; ++i) l[i] = __uint_as_float(rbuf[h & 1][i]);
                 } else {
-                    tmem_ld(lane_addr + acc * kN + h * kSub, l);
+                    if (!((VLC_K1_PROBE & 8) && h > 0)) tmem_ld(lane_addr + acc * kN + h * kSub, l);   // probe 8: one load per tile
                 }
                 if (h == kCh - 1) {
                     sm100::tc_fence_before();
@@ -386,7 +386,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                 for (int i = 0; i < kSub; ++i) l[i] = __uint_as_float(rbuf[h & 1][i]);
             } else {
-                tmem_ld(lane_addr + acc * kN + h * kSub, l);
+                if (!((VLC_K1_PROBE & 8) && h > 0)) tmem_ld(lane_addr + acc * kN + h * kSub, l);
             }
             if (h == kCh - 1) {
                 sm100::tc_fence_before();
