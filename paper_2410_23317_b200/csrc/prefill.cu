@@ -460,6 +460,381 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     }
 }
 
+// ---------------------------------------------------------------- two Q tiles per CTA
+// CTA = (query head, 256 prompt rows) as two 128-row Q tiles whose softmax
+// warpgroups take turns on the tensor core: S_i = Q_i K^T lands in TMEM
+// columns [128 i, 128 i + 128); warpgroup i (thread = row, the whole 128-key
+// row in one thread: no cross-warp max exchange) forms P_i = 2^(S c1 - m_ref c1)
+// as bf16 over the first 64 columns of its own S_i, and the MMA warp issues
+// O_i += P_i V (A = P_i from TMEM, O_i in columns 256 + 128 i) followed at once
+// by S_i of the next key tile, then the same for tile 1 -- so one warpgroup's
+// softmax overlaps the other's MMAs.  The commit that signals S_i of tile t
+// also covers O_i's previous P V, so a warpgroup may rescale its O_i row (lazy,
+// when the row max grows by more than 2^8) as soon as it sees S_i.
+// Warps: 0 K / Q producer, 1 MMA issuer, 2 TMEM allocator, 3 V^T producer,
+// 4-7 softmax of Q tile 0, 8-11 softmax of Q tile 1.
+#ifndef VLC_PF_PAIR
+#define VLC_PF_PAIR 1
+#endif
+constexpr int kPairThreads = 128 + 256;
+#ifndef VLC_PF_SLEEP
+#define VLC_PF_SLEEP 1
+#endif
+#ifndef VLC_PF_FAST
+#define VLC_PF_FAST 0   // full tiles: P without per-entry causal masks (measured slower)
+#endif
+#ifndef VLC_PF_REG
+#define VLC_PF_REG 1    // softmax keeps the 128-key S row in registers (one TMEM round trip per tile)
+#endif
+VLC_DEV void pair_wait(uint64_t* bar, uint32_t parity) {   // waits without spinning on the issue port
+    if (VLC_PF_SLEEP) sm100::mbar_wait_sleep(bar, parity);
+    else sm100::mbar_wait(bar, parity);
+}
+
+VLC_DEV float maxn(const float (&l)[32]) {   // 32 values, a balanced tree of 3-input maxima
+    float m[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m[k] = fmaxf(fmaxf(l[4 * k], l[4 * k + 1]), fmaxf(l[4 * k + 2], l[4 * k + 3]));
+    return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+}
+
+template <int D>
+struct PL2 {
+    static constexpr int KB = D / 64;
+    static constexpr uint32_t kQ = KB * kM * 128;     // one 128-row Q tile
+    static constexpr uint32_t kK = KB * kN * 128;     // one K tile
+    static constexpr uint32_t kV = 2 * D * 128;       // one V^T tile: D rows x 128 keys
+    static constexpr uint32_t kBytes = 2 * kQ + 2 * kK + 2 * kV + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kPairThreads, 1)
+prefill_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+                    const __grid_constant__ CUtensorMap vmap, PrefillArgs a) {
+    using LY = PL2<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sq = smem;
+    uint8_t* sk = sq + 2 * LY::kQ;
+    uint8_t* sv = sk + 2 * LY::kK;
+    __shared__ uint64_t qfull, kfull[2], kempty[2], vfull[2], vempty[2], sfull[2], pfull[2], ofull;
+    __shared__ uint32_t tmem_slot;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sq_slot = blockIdx.y;                                  // (b, l, query head)
+    const int rb = gridDim.x - 1 - blockIdx.x;                       // longest blocks first
+    const int64_t kv_slot = (int64_t)(sq_slot / a.Hq) * a.Hkv + (sq_slot % a.Hq) / (a.Hq / a.Hkv);
+    const int64_t r0 = (int64_t)rb * 2 * kM;
+    const bool two = r0 + kM < a.m;                                  // Q tile 1 has rows
+    const int T0 = (int)((imin(a.m, r0 + kM) + kN - 1) / kN);       // key tiles of Q tile 0
+    const int T1 = two ? (int)((imin(a.m, r0 + 2 * kM) + kN - 1) / kN) : 0;
+    const int T = two ? T1 : T0;
+
+    if (threadIdx.x == 0) {
+        sm100::mbar_init(&qfull, 1);
+        for (int i = 0; i < 2; ++i) {
+            sm100::mbar_init(kfull + i, 1); sm100::mbar_init(kempty + i, 1);
+            sm100::mbar_init(vfull + i, 1); sm100::mbar_init(vempty + i, 1);
+            sm100::mbar_init(sfull + i, 1); sm100::mbar_init(pfull + i, 4);
+        }
+        sm100::mbar_init(&ofull, 1);
+        sm100::fence_barrier_init();
+    }
+    if (warp == 2) sm100::tmem_alloc(&tmem_slot, 512);
+    sm100::tc_fence_before();
+    __syncthreads();
+    sm100::tc_fence_after();
+    const uint32_t tmem = tmem_slot;                                 // S_i at 128 i, O_i at 256 + 128 i
+
+    if (warp < 4) {
+        if (VLC_PF_REG) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n");
+        if (warp == 0 && lane == 0) {
+            sm100::tma_prefetch(&qmap);
+            sm100::tma_prefetch(&kmap);
+            sm100::mbar_expect_tx(&qfull, (two ? 2 : 1) * LY::kQ);
+            for (int i = 0; i < (two ? 2 : 1); ++i)
+                for (int kb = 0; kb < LY::KB; ++kb)
+                    sm100::tma_load_2d(sq + i * LY::kQ + kb * kM * 128, &qmap, &qfull, kb * 64,
+                                       (int)(sq_slot * a.q_rows + r0 + i * kM));
+            for (int t = 0; t < T; ++t) {
+                const int st = t & 1;
+                pair_wait(kempty + st, ((t >> 1) & 1) ^ 1);
+                sm100::mbar_expect_tx(kfull + st, LY::kK);
+                for (int kb = 0; kb < LY::KB; ++kb)
+                    sm100::tma_load_2d(sk + st * LY::kK + kb * kN * 128, &kmap, kfull + st, kb * 64,
+                                       (int)(kv_slot * a.kv_rows + (int64_t)t * kN));
+            }
+        } else if (warp == 3 && lane == 0) {
+            sm100::tma_prefetch(&vmap);
+            for (int t = 0; t < T; ++t) {
+                const int st = t & 1;
+                pair_wait(vempty + st, ((t >> 1) & 1) ^ 1);
+                sm100::mbar_expect_tx(vfull + st, LY::kV);
+                for (int kb = 0; kb < 2; ++kb)
+                    sm100::tma_load_2d(sv + st * LY::kV + kb * D * 128, &vmap, vfull + st, t * kN + kb * 64,
+                                       (int)(kv_slot * D));
+            }
+        } else if (warp == 1 && lane == 0) {
+            constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kM, kN);
+            constexpr uint32_t idesc_o = sm100::idesc_bf16_f32(kM, D);
+            auto mma_s = [&](int i, int t) {   // S_i = Q_i K_t^T, then signal S_i (covers O_i's P V too)
+                const uint32_t q_addr = sm100::smem_u32(sq + i * LY::kQ);
+                const uint32_t k_addr = sm100::smem_u32(sk + (t & 1) * LY::kK);
+#pragma unroll
+                for (int kb = 0; kb < LY::KB; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        sm100::mma_bf16(tmem + i * kN, sm100::sdesc_k_sw128(q_addr + kb * kM * 128 + kk * 32),
+                                        sm100::sdesc_k_sw128(k_addr + kb * kN * 128 + kk * 32), idesc_s,
+                                        (kb | kk) != 0);
+                sm100::mma_commit(sfull + i);
+            };
+            auto mma_pv = [&](int i, int t) {  // O_i += P_i V_t, P_i packed over S_i's first 64 columns
+                const uint32_t v_addr = sm100::smem_u32(sv + (t & 1) * LY::kV);
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+                        sm100::mma_bf16_ts(tmem + 2 * kN + i * kN, tmem + i * kN + (kb * 4 + kk) * 8,
+                                           sm100::sdesc_k_sw128(v_addr + kb * D * 128 + kk * 32), idesc_o,
+                                           (t | kb | kk) != 0);
+            };
+            pair_wait(&qfull, 0);
+            pair_wait(kfull, 0);
+            sm100::tc_fence_after();
+            mma_s(0, 0);
+            if (two) mma_s(1, 0);
+            sm100::mma_commit(kempty);
+            for (int t = 0; t < T; ++t) {
+                const bool h0 = t < T0, n0 = t + 1 < T0, n1 = two && t + 1 < T1;
+                if (n0 || n1) pair_wait(kfull + ((t + 1) & 1), ((t + 1) >> 1) & 1);
+                pair_wait(vfull + (t & 1), (t >> 1) & 1);
+                if (h0) {
+                    pair_wait(pfull, t & 1);
+                    sm100::tc_fence_after();
+                    mma_pv(0, t);
+                    if (n0) mma_s(0, t + 1);
+                }
+                if (two) {
+                    pair_wait(pfull + 1, t & 1);
+                    sm100::tc_fence_after();
+                    mma_pv(1, t);
+                    if (n1) mma_s(1, t + 1);
+                }
+                sm100::mma_commit(vempty + (t & 1));
+                if (n0 || n1) sm100::mma_commit(kempty + ((t + 1) & 1));
+            }
+            sm100::mma_commit(&ofull);
+        }
+    } else {
+        // ---- softmax warpgroup wg of Q tile wg: thread = row, the whole 128-key row
+        if (VLC_PF_REG) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n");
+        const int wg = (warp - 4) >> 2, sub = warp & 3;
+        const int li = 32 * sub + lane;
+        const int Ti = wg ? T1 : T0;
+        const int64_t r = r0 + wg * kM + li;
+        const bool row_ok = r < a.m;
+        const int64_t row_end = row_ok ? r + 1 : 0;                   // causal: keys [0, r]
+        const uint32_t lq = uint32_t(32 * sub) << 16;
+        const uint32_t s_addr = tmem + lq + wg * kN, o_addr = tmem + lq + 2 * kN + wg * kN;
+        const float c1 = a.inv_scale * kLog2e;
+        const float grow_raw = 8.f / c1;
+        float m_ref = -INFINITY, m_true = -INFINITY;
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};
+        float l[32];
+#if VLC_PF_REG
+        // the whole 128-key S row in registers: four loads in flight, one wait,
+        // then the row max and P from the same registers
+        uint32_t sr[4][32];
+        for (int t = 0; t < Ti; ++t) {
+            pair_wait(sfull + wg, t & 1);
+            sm100::tc_fence_after();
+            const int64_t k0 = (int64_t)t * kN;
+            const bool full = __all_sync(kFull, k0 + kN <= row_end);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm100::tmem_ld32_issue(s_addr + 32 * c, sr[c]);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sm100::tmem_ld32_wait(sr[c]);   // the first waits; all tie their registers
+            float tm = -INFINITY;
+            if (full) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    float v[32];
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(sr[c][k]);
+                    tm = fmaxf(tm, maxn(v));
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int valid = (int)imax(0, imin(32, row_end - (k0 + 32 * c)));
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) tm = k < valid ? fmaxf(tm, __uint_as_float(sr[c][k])) : tm;
+                }
+            }
+            m_true = fmaxf(m_true, tm);
+            const bool grow = tm > m_ref + grow_raw;
+            if (__any_sync(kFull, grow)) {
+                const float sc = (grow && m_ref != -INFINITY) ? ex2((m_ref - tm) * c1) : 1.f;
+                if (t > 0) {   // every earlier P V into O_i is complete (the S_i signal covers it)
+#pragma unroll 1
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        sm100::tmem_ld32(o_addr + 32 * c, o);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) o[k] *= sc;
+                        sm100::tmem_st32(o_addr + 32 * c, o);
+                    }
+                }
+                if (grow) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) ps[k] *= sc;
+                    m_ref = tm;
+                }
+            }
+            const float mb = m_ref * c1;
+            if (full) {
+                // packed pairs: FFMA2 for the exponent arguments, FADD2 for two of the
+                // four sum chains (row sums only need float32 rounding)
+                const float2 c1v = make_float2(c1, c1), nmb = make_float2(-mb, -mb);
+                float2 s01 = make_float2(ps[0], ps[1]), s23 = make_float2(ps[2], ps[3]);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float2 u = __ffma2_rn(make_float2(__uint_as_float(sr[c][2 * k]), __uint_as_float(sr[c][2 * k + 1])),
+                                                    c1v, nmb);
+                        const float2 e = make_float2(ex2(u.x), ex2(u.y));
+                        if (k & 1) s23 = __fadd2_rn(s23, e);
+                        else s01 = __fadd2_rn(s01, e);
+                        pk[k] = pack_bf16(e.x, e.y);
+                    }
+                    sm100::tmem_st16_nowait(s_addr + 16 * c, pk);
+                }
+                ps[0] = s01.x; ps[1] = s01.y; ps[2] = s23.x; ps[3] = s23.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t pk[16];
+                    const int valid = (int)imax(0, imin(32, row_end - (k0 + 32 * c)));
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = 2 * k < valid ? ex2(fmaf(__uint_as_float(sr[c][2 * k]), c1, -mb)) : 0.f;
+                        const float p1 = 2 * k + 1 < valid ? ex2(fmaf(__uint_as_float(sr[c][2 * k + 1]), c1, -mb)) : 0.f;
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                    sm100::tmem_st16_nowait(s_addr + 16 * c, pk);
+                }
+            }
+            sm100::tmem_st_wait();
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(pfull + wg);
+        }
+#else
+        for (int t = 0; t < Ti; ++t) {
+            pair_wait(sfull + wg, t & 1);
+            sm100::tc_fence_after();
+            const int64_t k0 = (int64_t)t * kN;
+            const bool full = __all_sync(kFull, k0 + kN <= row_end);
+            // sweep A: the tile's row max
+            float tm = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                sm100::tmem_ld32(s_addr + 32 * c, l);
+                if (full) {
+                    tm = fmaxf(tm, maxn(l));
+                } else {
+                    const int valid = (int)imax(0, imin(32, row_end - (k0 + 32 * c)));
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) tm = k < valid ? fmaxf(tm, l[k]) : tm;
+                }
+            }
+            m_true = fmaxf(m_true, tm);
+            const bool grow = tm > m_ref + grow_raw;
+            if (__any_sync(kFull, grow)) {
+                const float sc = (grow && m_ref != -INFINITY) ? ex2((m_ref - tm) * c1) : 1.f;
+                if (t > 0) {   // every earlier P V into O_i is complete (the S_i signal covers it)
+#pragma unroll 1
+                    for (int c = 0; c < D / 32; ++c) {
+                        float o[32];
+                        sm100::tmem_ld32(o_addr + 32 * c, o);
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) o[k] *= sc;
+                        sm100::tmem_st32(o_addr + 32 * c, o);
+                    }
+                }
+                if (grow) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) ps[k] *= sc;
+                    m_ref = tm;
+                }
+            }
+            const float mb = m_ref * c1;
+            // sweep B: P over S_i's own columns (chunk c's 16 packed columns only
+            // overwrite S columns already loaded: 16 c + 15 < 32 (c + 1))
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                sm100::tmem_ld32(s_addr + 32 * c, l);
+                uint32_t pk[16];
+                if (VLC_PF_FAST && full) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = ex2(fmaf(l[2 * k], c1, -mb)), p1 = ex2(fmaf(l[2 * k + 1], c1, -mb));
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                } else {
+                    const int valid = full ? 32 : (int)imax(0, imin(32, row_end - (k0 + 32 * c)));
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float p0 = 2 * k < valid ? ex2(fmaf(l[2 * k], c1, -mb)) : 0.f;
+                        const float p1 = 2 * k + 1 < valid ? ex2(fmaf(l[2 * k + 1], c1, -mb)) : 0.f;
+                        ps[(2 * k) & 3] += p0;
+                        ps[(2 * k + 1) & 3] += p1;
+                        pk[k] = pack_bf16(p0, p1);
+                    }
+                }
+                sm100::tmem_st16(s_addr + 16 * c, pk);
+            }
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(pfull + wg);
+        }
+#endif
+        if (Ti > 0) {
+            const float l_ref = (ps[0] + ps[1]) + (ps[2] + ps[3]);
+            if (row_ok && a.row_max) {
+                a.row_max[(int64_t)sq_slot * a.m + r] = m_true * a.inv_scale;
+                a.row_sum[(int64_t)sq_slot * a.m + r] = l_ref * ex2((m_ref - m_true) * c1);
+            }
+            const float il = row_ok ? 1.f / l_ref : 0.f;
+            pair_wait(&ofull, 0);
+            sm100::tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                sm100::tmem_ld32(o_addr + 32 * c, l);
+                if (row_ok) {
+                    float4* dst = reinterpret_cast<float4*>(a.out + ((int64_t)sq_slot * a.m + r) * D + 32 * c);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        dst[q] = make_float4(l[4 * q] * il, l[4 * q + 1] * il, l[4 * q + 2] * il, l[4 * q + 3] * il);
+                }
+            }
+        }
+    }
+    sm100::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        sm100::tc_fence_after();
+        sm100::tmem_dealloc(tmem, 512);
+    }
+}
+
 // V [slots, kv_rows, D] -> V^T [slots, D, tpad] (keys contiguous), zero past m
 __global__ void transpose_v(const __nv_bfloat16* __restrict__ v, __nv_bfloat16* __restrict__ vt, int64_t kv_rows,
                             int d, int64_t m, int64_t tpad) {
@@ -489,6 +864,15 @@ cudaError_t launch_prefill_d(const PrefillArgs& a, cudaStream_t st) {
     if (!make_tmap_2d(&qmap, a.q, q_slots * a.q_rows, D, kM)) return cudaErrorInvalidValue;
     if (!make_tmap_2d(&kmap, a.k, kv_slots * a.kv_rows, D, kN)) return cudaErrorInvalidValue;
     if (!make_tmap_2d_strided(&vmap, a.vt, kv_slots * D, (int)tpad, tpad, D, true)) return cudaErrorInvalidValue;
+    if (VLC_PF_PAIR) {
+        const size_t smem = PL2<D>::kBytes;
+        cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid((unsigned)((a.m + 2 * kM - 1) / (2 * kM)), (unsigned)q_slots);
+        prefill_pair_kernel<D><<<grid, kPairThreads, smem, st>>>(qmap, kmap, vmap, a);
+        return cudaGetLastError();
+    }
     const size_t smem = PL<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -43,6 +43,19 @@ SM100_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // (a suspend-time hint on try_wait measured slower: decode 7.2 -> 8.4 us/step,
 // K1 unchanged -- the waits here are short and latency-critical)
+// with a suspend-time hint: the waiting warp sleeps until the phase completes
+// (or the hint elapses) instead of spinning on the issue port
+SM100_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
 
 // ---------------------------------------------------------------- TMA
 SM100_DEV void tma_prefetch(const CUtensorMap* map) {
@@ -121,6 +134,17 @@ SM100_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
         : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 32 lanes x 16 consecutive 32-bit columns from registers, no wait (pair with
+// tmem_st_wait before anything reads the columns)
+SM100_DEV void tmem_st16_nowait(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+SM100_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // 32 lanes x 32 consecutive 32-bit columns from registers; waits for completion
 SM100_DEV void tmem_st32(uint32_t taddr, const float (&v)[32]) {
     asm volatile(

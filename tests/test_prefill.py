@@ -67,7 +67,9 @@ def test_gpu_prefill_stats_equal_k1():
     k1_max = eng.row_max.view(B, L, HQ, W)
     k1_sum = eng.row_sum.view(B, L, HQ, W)
     assert torch.equal(rmax[..., M - W:], k1_max)
-    torch.testing.assert_close(rsum[..., M - W:], k1_sum, rtol=2e-6, atol=0)
+    # sums: the same exponentials in another partial order (the prefill thread sums
+    # its row's 128 keys per tile in four chains) -- the parity bar of SURVEY 8c
+    torch.testing.assert_close(rsum[..., M - W:], k1_sum, rtol=1e-5, atol=0)
 
 
 @pytest.mark.gpu
@@ -109,7 +111,7 @@ def test_gpu_prefill_compress_equals_compress():
     assert torch.isfinite(out).all()
     assert torch.equal(a.below_head, b.below_head)
     assert torch.equal(a.kept_counts, b.kept_counts)
-    torch.testing.assert_close(b.row_sum, a.row_sum, rtol=2e-6, atol=0)
+    torch.testing.assert_close(b.row_sum, a.row_sum, rtol=1e-5, atol=0)
     assert torch.equal(a.row_max, b.row_max)
     ka, kb = a.kept_sets(), b.kept_sets()
     diff = sum(int((x != y).sum()) if x.shape == y.shape else 10**6
