@@ -57,7 +57,7 @@ constexpr int kStages = VLC_DEC_STAGES;
 #define VLC_DEC_L2PF 0   // L2 bulk prefetch of the rows beyond the first ring (measured slower: 7.28 vs 7.12 us/step, B8 72.5 vs 66.6)
 #endif
 #ifndef VLC_DEC_PROBE
-#define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring
+#define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring, 4 = no wait for the previous step, 8 = no merge / output
 #endif
 
 template <int D>
@@ -166,7 +166,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     bool waited = !a.chained;
     auto wait_prev = [&]() {
         if (!waited) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (!(VLC_DEC_PROBE & 4)) asm volatile("griddepcontrol.wait;" ::: "memory");   // probe 4: no wait (racy)
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
             waited = true;
         }
@@ -328,6 +328,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     }
 
     wait_prev();                                              // before the output writes
+    if (VLC_DEC_PROBE & 8) return;                            // probe 8: no merge, no output
     // ---- merge the warps: per head, (max, sum) then O, through shared memory
 #pragma unroll
     for (int o2 = 4; o2 < 32; o2 <<= 1) {
@@ -339,18 +340,23 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         part_m[warp][2 * quad + 1] = run_m[1]; part_s[warp][2 * quad + 1] = run_s[1];
     }
     __syncthreads();                                          // both groups are done with the ring
-    float* po = reinterpret_cast<float*>(smem);               // [kWarps][8 heads][D], ring is idle now
+    if (VLC_DEC_PROBE & 32) return;                           // probe 32: only the first merge barrier
+    // O partials as [warp][dim][8 heads]: a thread's two adjacent heads are one
+    // 8-byte store and a warp's stores cover 64 consecutive floats (no bank
+    // conflicts); the padding heads >= G are not stored at all
+    float* po = reinterpret_cast<float*>(smem);               // ring is idle now
+    if (2 * quad < G) {
 #pragma unroll
-    for (int t = 0; t < C::MT; ++t) {
-        const int d0 = 16 * t + row;
-        po[(warp * 8 + 2 * quad) * D + d0] = o[t][0];
-        po[(warp * 8 + 2 * quad + 1) * D + d0] = o[t][1];
-        po[(warp * 8 + 2 * quad) * D + d0 + 8] = o[t][2];
-        po[(warp * 8 + 2 * quad + 1) * D + d0 + 8] = o[t][3];
+        for (int t = 0; t < C::MT; ++t) {
+            const int d0 = 16 * t + row;
+            *reinterpret_cast<float2*>(po + (warp * D + d0) * 8 + 2 * quad) = make_float2(o[t][0], o[t][1]);
+            *reinterpret_cast<float2*>(po + (warp * D + d0 + 8) * 8 + 2 * quad) = make_float2(o[t][2], o[t][3]);
+        }
     }
     __syncthreads();
+    if (VLC_DEC_PROBE & 16) return;                           // probe 16: no final combine / output
     for (int idx = tid; idx < G * D; idx += kThreads) {
-        const int g = idx / D, dim = idx % D;
+        const int g = idx % G, dim = idx / G;
         float M = -INFINITY;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) M = fmaxf(M, part_m[w][g]);
@@ -360,7 +366,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             if (part_m[w][g] == -INFINITY) continue;
             const float f = ex2((part_m[w][g] - M) * c1);
             S = fmaf(part_s[w][g], f, S);
-            O = fmaf(po[(w * 8 + g) * D + dim], f, O);
+            O = fmaf(po[(w * D + dim) * 8 + g], f, O);
         }
         a.out[((int64_t)s * G + g) * D + dim] = O / S;
     }
