@@ -70,14 +70,15 @@ VLC_API int64_t vlc_score_partials(int64_t rows);
  * from float64 dots exactly as the reference computes them, so below counts
  * and row_max equal the reference's for bf16-representable inputs.
  * exact_ws: 256-byte aligned, >= vlc_score_exact_bytes(slots, group, window,
- * E) bytes for room for E listed entries (E >= slots*G*w is ample; beyond
- * capacity the fp32 decision is kept).  After the call (stream-ordered) its
+ * E) bytes for room for E listed chunks (a key x 32 window rows each; E >=
+ * slots*G*w is ample; beyond capacity the fp32 decisions are kept).  After the call (stream-ordered) its
  * first 32 bytes hold the status words, int32 unless noted:
- *   [0] entries deferred to an exact row max   [1] entries listed by K1
- *   [2] OVERFLOW: listed entries that kept the fp32 decision (list full; the
- *       below counts may then differ from the reference's)
+ *   [0] entries deferred to an exact row max   [1] chunks listed by K1
+ *   [2] OVERFLOW: chunks that found the list full (their near-threshold
+ *       entries stay undecided: the below counts may differ from the reference's)
  *   [3] rows whose exact max was recomputed    [4] keys the row scan listed
- *   [5] f32: largest observed |tensor-core logit - exact logit| (listed entries)
+ *   [5] f32: largest observed difference between a listed chunk's smallest
+ *       |logit - threshold| from the tensor cores and from float64 (logit units)
  *   [6] f32: largest observed |fp32 row max - exact row max| (recomputed rows)
  * [5] and [6] check the margins exact mode relies on (VLC_EXACT_BAND_LOGIT,
  * VLC_EXACT_ROWMAX_ERR): callers treat [5] + [6] > VLC_EXACT_BAND_LOGIT / 8

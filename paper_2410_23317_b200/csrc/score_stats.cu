@@ -60,34 +60,48 @@ VLC_DEV void add_below(const ScoreArgs& a, const int4& e) {
     if (a.below_col) atomicAdd(a.below_col + (int64_t)e.x * a.n + e.z, e.w);
 }
 
-// 1: decide each listed entry against K1's row max; undecidable ones (within
-// the row max's own error of the threshold) wait for the exact row max.  The
-// exact logit travels in the waiting entry's .w (its weight is always 1).
+// 1: K1 listed chunks -- key j x kSub consecutive window rows (.y = the first)
+// -- holding an entry within its band of a decision.  One warp per chunk,
+// lane = row: each entry gets its exact logit and is decided against K1's row
+// max, or waits for the exact row max when within that max's own error of the
+// threshold (the exact logit travels in the waiting entry's .w).  Lane 0
+// compares the chunk's smallest exact |u| with the tensor-core one K1 saw
+// (the runtime margin check).
 template <int D>
 __global__ void fix_flags(ScoreArgs a) {
     pdl_wait_then_release();
     const int n = min(a.fix_counts[1], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x / 32;
+    for (int i = blockIdx.x * wpb + threadIdx.x / 32; i < n; i += gridDim.x * wpb) {
         const int4 f = a.flag[i];
-        const int4 e = make_int4(f.x, f.y, f.z, 1);
-        const int64_t rr = (int64_t)e.x * R + e.y;
-        const float l = exact_logit<D>(a, e.x, e.y, e.z);
-        // the tensor-core logit's observed error (the margins' runtime check)
-        atomicMax(reinterpret_cast<unsigned*>(a.fix_counts + 5), __float_as_uint(fabsf(l - __int_as_float(f.w) * a.inv_scale)));
-        const float x = l - a.row_max[rr];
-        if (x < a.t_star - a.err_max) {
-            add_below(a, e);
-        } else if (x < a.t_star + a.err_max) {
-            const int at = atomicAdd(a.fix_counts, 1);
-            if (at < a.cap) {
-                a.cand[at] = make_int4(e.x, e.y, e.z, __float_as_int(l));
-            } else {   // no room: decide against the fp32 row max
-                atomicAdd(a.fix_counts + 2, 1);
-                if (x < a.t_star) add_below(a, e);
+        const int row = f.y + lane;
+        const bool ok = lane < kScoreSub && row < R && f.z <= a.q_base + (row % a.w) && f.z < a.n;
+        float minu = INFINITY;
+        if (ok) {
+            const int4 e = make_int4(f.x, row, f.z, 1);
+            const int64_t rr = (int64_t)e.x * R + e.y;
+            const float l = exact_logit<D>(a, e.x, e.y, e.z);
+            const float x = l - a.row_max[rr];
+            minu = fabsf((x - a.t_star) * kLog2e);
+            if (x < a.t_star - a.err_max) {
+                add_below(a, e);
+            } else if (x < a.t_star + a.err_max) {
+                const int at = atomicAdd(a.fix_counts, 1);
+                if (at < a.cap) {
+                    a.cand[at] = make_int4(e.x, e.y, e.z, __float_as_int(l));
+                } else {   // no room: decide against the fp32 row max
+                    atomicAdd(a.fix_counts + 2, 1);
+                    if (x < a.t_star) add_below(a, e);
+                }
+                if (atomicExch(a.rmax_key + rr, 1u) == 0u) a.rows[atomicAdd(a.fix_counts + 3, 1)] = (int)rr;
             }
-            if (atomicExch(a.rmax_key + rr, 1u) == 0u) a.rows[atomicAdd(a.fix_counts + 3, 1)] = (int)rr;
         }
+        minu = warp_min(minu);
+        if (lane == 0 && minu != INFINITY)
+            atomicMax(reinterpret_cast<unsigned*>(a.fix_counts + 5),
+                      __float_as_uint(fabsf(minu - __int_as_float(f.w)) / kLog2e));
     }
 }
 
@@ -213,7 +227,7 @@ __global__ void fix_deferred(ScoreArgs a) {
 
 template <int D>
 cudaError_t launch_fixups(const ScoreArgs& a, cudaStream_t st) {
-    cudaError_t e = launch_pdl(fix_flags<D>, dim3(296), dim3(256), 0, st, a);
+    cudaError_t e = launch_pdl(fix_flags<D>, dim3(592), dim3(256), 0, st, a);
     if (e == cudaSuccess) e = launch_pdl(fix_rowscan<D>, dim3(24, 148), dim3(256), 0, st, a);
     if (e == cudaSuccess) e = launch_pdl(fix_rowmax<D>, dim3(296), dim3(256), 0, st, a);
     if (e == cudaSuccess) e = launch_pdl(fix_deferred, dim3(148), dim3(256), 0, st, a);

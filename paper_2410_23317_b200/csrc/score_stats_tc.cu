@@ -110,7 +110,7 @@ VLC_DEV void tmem_wait(uint32_t (&r)[N]) {
 #endif
 constexpr bool kPipe = VLC_K1_PIPE;   // software-pipelined TMEM loads in the epilogue
 #ifndef VLC_K1_PROBE
-#define VLC_K1_PROBE 0   // timing probes (wrong results), bits: 1 = no epilogue math, 2 = no MMA, 4 = no TMA after the first ring, 8 = one TMEM load per tile
+#define VLC_K1_PROBE 0   // timing probes (wrong results), bits: 1 = no epilogue math, 2 = no MMA, 4 = no TMA after the first ring, 8 = one TMEM load per tile, 16 = exact mode without its listing path
 #endif
 
 template <int D, bool EXACT>
@@ -432,27 +432,24 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                     else cs01 = __ffma2_rn(e, make_float2(c.z, c.w), cs01);
                 }
             }
-            const float cntf = cf.x + cf.y;
-            if (EXACT && __any_sync(kFull, minabs < band)) {
-                // list this thread's in-band entries (one atomic reserves them all)
-                int nf = 0;
-#pragma unroll
-                for (int k = 0; k < kSub; ++k) {
-                    const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
-                    nf += (j < a.n && j <= c_lim[rh + k] && fabsf(u) < band) ? 1 : 0;
-                }
-                int at = nf ? atomicAdd(a.fix_counts + 1, nf) : 0;
-#pragma unroll
-                for (int k = 0; k < kSub; ++k) {   // static indices: l stays in registers
-                    const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
-                    if (nf && j < a.n && j <= c_lim[rh + k] && fabsf(u) < band) {
-                        if (at < a.cap) {
-                            a.flag[at] = make_int4(s, (int)(r_first + rh + k), j, __float_as_int(l[k]));   // .w: the fp32 dot
-                        } else {   // list full: keep the fp32 decision (reported as overflow)
-                            atomicAdd(a.fix_counts + 2, 1);
-                            cnt += u < 0.f ? 1 : 0;
-                        }
-                        ++at;
+            float cntf = cf.x + cf.y;
+            // exact mode: a lane whose chunk holds an entry within `band` of its
+            // decision lists the whole chunk (key j x these kSub rows) in one record
+            // and counts none of it here; the fix-up re-decides all of its entries
+            // from float64 dots.  No per-entry work on this path: l[] is dead here.
+            bool listed = false;
+            if (EXACT && !(VLC_K1_PROBE & 16) && __any_sync(kFull, minabs < band)) {
+                if (j < a.n && minabs < band) {
+                    const int at = atomicAdd(a.fix_counts + 1, 1);
+                    if (at < a.cap) {
+                        // .w: the chunk's smallest |u| from the tensor-core logits (log2
+                        // units), which the fix-up compares with the exact one
+                        a.flag[at] = make_int4(s, (int)(r_first + rh), j, __float_as_int(minabs));
+                        listed = true;
+                        cntf = 0.f;
+                    } else {   // list full: keep the fp32 decisions (reported as overflow)
+                        atomicAdd(a.fix_counts + 2, 1);
+                        cntf += 0.f;   // entries in the band stay uncounted: the overflow raises
                     }
                 }
             }
@@ -461,7 +458,7 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
 #pragma unroll
                 for (int k = 0; k < kSub; ++k) {
                     const float u = fmaf(l[k], c1, -(reinterpret_cast<const float*>(pk4 + (k >> 1))[k & 1]));
-                    const int tot = __reduce_add_sync(kFull, (j <= c_lim[rh + k] && u < -band) ? 1 : 0);
+                    const int tot = __reduce_add_sync(kFull, (!listed && j <= c_lim[rh + k] && u < -band) ? 1 : 0);
                     if (lane == 0 && tot) atomicAdd(hcnt + (int)((r_first + rh + k) / a.w - head0), tot);
                 }
             }

@@ -81,6 +81,11 @@ VLC_DEV float warp_max(float x) {
     for (int o = 16; o >= 1; o >>= 1) x = fmaxf(x, __shfl_xor_sync(kFull, x, o));
     return x;
 }
+VLC_DEV float warp_min(float x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x = fminf(x, __shfl_xor_sync(kFull, x, o));
+    return x;
+}
 
 // Inclusive block scan (sum) of one value per thread; blockDim.x <= 1024,
 // multiple of 32.  `scratch` holds >= 32 entries.

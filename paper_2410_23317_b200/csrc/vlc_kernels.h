@@ -27,6 +27,13 @@ int exact_ws_cap(int64_t bytes, int64_t slots, int64_t rows);    // <= 0: too sm
 // K1: post-vision attention statistics for every (b, l, kv) slot.
 // Slot s = (b*L + l)*Hkv + kv owns window rows [s*R, s*R + R), R = G*w, i.e.
 // heads kv*G .. kv*G+G-1 of the [B, L, Hq, w, d] window tensor.
+// K1's epilogue chunk: TMEM columns a thread holds at a time, and so the rows of
+// one exact-mode listing record (score_stats_tc.cu, score_stats.cu)
+#ifndef VLC_K1_SUB
+#define VLC_K1_SUB 32
+#endif
+constexpr int kScoreSub = VLC_K1_SUB;
+
 struct ScoreArgs {
     const void* q;          // bf16 [B*L*Hq, w, d]   (window query rows)
     const void* k;          // bf16 [B*L*Hkv, T, d]  (keys; rows >= n never read)

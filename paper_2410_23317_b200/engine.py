@@ -478,11 +478,12 @@ class VLCache:
 
     # ------------------------------------------------------------ results
     def exact_stats(self) -> dict:
-        """Exact mode's counters from the last K1 call (synchronises): entries
-        K1 listed for a float64 re-decision, those deferred to an exact row
-        max, rows scanned for it, and `overflow` -- listed entries that found
-        the list full and kept K1's fp32 decision (their below count may then
-        differ from the reference's).  Empty when exact mode is off."""
+        """Exact mode's counters from the last K1 call (synchronises): chunks
+        (a key x 32 window rows) K1 listed for a float64 re-decision, entries
+        deferred to an exact row max, rows scanned for it, `overflow` -- chunks
+        that found the list full (their below counts may then differ from the
+        reference's) -- and the observed tensor-core errors against exact
+        mode's margins.  Empty when exact mode is off."""
         import torch
 
         if self.exact_ws is None:
