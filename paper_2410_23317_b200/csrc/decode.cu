@@ -345,6 +345,20 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     // 8-byte store and a warp's stores cover 64 consecutive floats (no bank
     // conflicts); the padding heads >= G are not stored at all
     float* po = reinterpret_cast<float*>(smem);               // ring is idle now
+    __shared__ float f_s[kWarps][8], is_s[8];                 // per (warp, head) rescale, 1 / sum per head
+    if (tid < G) {   // the merge's scalars once per head, not once per output
+        float M = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, part_m[w][tid]);
+        float S = 0.f;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const float f = part_m[w][tid] == -INFINITY ? 0.f : ex2((part_m[w][tid] - M) * c1);
+            f_s[w][tid] = f;
+            S = fmaf(part_s[w][tid], f, S);
+        }
+        is_s[tid] = 1.f / S;
+    }
     if (2 * quad < G) {
 #pragma unroll
         for (int t = 0; t < C::MT; ++t) {
@@ -357,18 +371,10 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     if (VLC_DEC_PROBE & 16) return;                           // probe 16: no final combine / output
     for (int idx = tid; idx < G * D; idx += kThreads) {
         const int g = idx % G, dim = idx / G;
-        float M = -INFINITY;
+        float O = 0.f;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) M = fmaxf(M, part_m[w][g]);
-        float S = 0.f, O = 0.f;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            if (part_m[w][g] == -INFINITY) continue;
-            const float f = ex2((part_m[w][g] - M) * c1);
-            S = fmaf(part_s[w][g], f, S);
-            O = fmaf(po[(w * D + dim) * 8 + g], f, O);
-        }
-        a.out[((int64_t)s * G + g) * D + dim] = O / S;
+        for (int w = 0; w < kWarps; ++w) O = fmaf(po[(w * D + dim) * 8 + g], f_s[w][g], O);
+        a.out[((int64_t)s * G + g) * D + dim] = O * is_s[g];
     }
 }
 
