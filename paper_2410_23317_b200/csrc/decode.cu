@@ -5,12 +5,14 @@
 // KV head) and _core.pyx:245-278 (decode_step: softmax(q K^T / sqrt(d)) V, fp32).
 //
 // One CTA per (b, l, kv) slot streams the slot's K and V rows through a
-// kStages-deep shared-memory ring of 64-row chunks, loaded by 2-D TMA with the
+// 6-stage shared-memory ring of 32-row chunks, loaded by 2-D TMA with the
 // 128-byte swizzle so tensor-core fragments come out of shared memory
-// conflict-free.  Two groups of four warps take alternate chunks (group c % 2
-// consumes chunk c), so two chunks are in compute at once and the serial
-// chain of the slot's longest-budget layers is halved; inside a group warp w
-// owns rows 16w .. 16w+15 of the chunk.  The G <= 8 query heads of the KV head
+// conflict-free.  Four groups of two warps take chunks round robin (group
+// c % 4 consumes chunk c), so four chunks are in compute at once and the
+// serial chain of the slot's longest-budget layers is a quarter; inside a
+// group warp w owns rows 16w .. 16w+15 of the chunk.  (Round 1 used two
+// groups of four warps on 64-row chunks in a 3-stage ring: 6.68 vs 6.61
+// us/step at M7B, 63.4 vs 62.2 at batch 8.)  The G <= 8 query heads of the KV head
 // are the N = 8 columns of transposed mma.sync tiles (GQA: every key row is
 // read from HBM once per step for the whole group; no padding of the big M side):
 //   S^T = K Q^T    m16n8k16, M = 16 keys, bf16 in, fp32 accumulate (exact products);
@@ -22,7 +24,7 @@
 // the chunk holding the previous step's append (and the global writes) wait
 // for the previous step: everything else is loaded and computed while it
 // drains.  Each stage has two full barriers used alternately, so a group that
-// runs a ring ahead of the other never mistakes a stage's previous use for its
+// runs a ring ahead of another never mistakes a stage's previous use for its
 // chunk.  A stage is refilled as soon as the four
 // warps that consumed it arrive on its "empty" barrier.  The chunk holding row
 // k + step takes it from k_new / v_new (patched into the swizzled tile) and
@@ -35,10 +37,10 @@ namespace vlc {
 namespace {
 
 #ifndef VLC_DEC_GROUP_WARPS
-#define VLC_DEC_GROUP_WARPS 4
+#define VLC_DEC_GROUP_WARPS 2
 #endif
 #ifndef VLC_DEC_GROUPS
-#define VLC_DEC_GROUPS 2
+#define VLC_DEC_GROUPS 4
 #endif
 constexpr int kGroupWarps = VLC_DEC_GROUP_WARPS;   // warps per consumer group (16 rows each)
 constexpr int kGroups = VLC_DEC_GROUPS;            // groups take chunks round-robin
@@ -47,7 +49,7 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kMaxG = 8;
 constexpr int kChunk = 16 * kGroupWarps;        // rows per ring stage
 #ifndef VLC_DEC_STAGES
-#define VLC_DEC_STAGES 3
+#define VLC_DEC_STAGES 6   // >= VLC_DEC_GROUPS: a group runs at most one use of a stage ahead
 #endif
 constexpr int kStages = VLC_DEC_STAGES;
 #ifndef VLC_DEC_SCHAINS
