@@ -22,6 +22,15 @@ int score_partials(int64_t rows) { return (int)(2 * ((rows + 127) / 128)); }
 
 namespace {
 
+#ifndef VLC_RS_X
+#define VLC_RS_X 24   // exact row scan: blocks per row
+#endif
+#ifndef VLC_RS_Y
+#define VLC_RS_Y 148  // rows in flight
+#endif
+#ifndef VLC_RS_U
+#define VLC_RS_U 4    // keys per half-warp in flight
+#endif
 constexpr int64_t kAlign = 256;
 int64_t up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(256) fix_rowscan(ScoreArgs a) {
         const uint4 qv = qrow[sub];
         const uint32_t qa[4] = {qv.x, qv.y, qv.z, qv.w};
         float mx = -INFINITY;
-        constexpr int kU = 4;   // keys per half-warp in flight
+        constexpr int kU = VLC_RS_U;   // keys per half-warp in flight
         for (int64_t j0 = kslot0 - grp; j0 < lim; j0 += kU * kstride) {   // warp-uniform trip count
             uint4 kv[kU];
             const uint4* krow[kU];
@@ -178,11 +187,20 @@ __global__ void __launch_bounds__(256) fix_rowscan(ScoreArgs a) {
                     sa += __shfl_xor_sync(kFull, sa, o);
                 }
                 const float hi = (f + 2.f * kRel * sa) * a.inv_scale;
-                if (j < lim && sub == 0 && hi >= floor_logit - fabsf(floor_logit) * 1e-6f) {
-                    // list it (the flag list is free once fix_flags ran); scored in parallel next
-                    const int at = atomicAdd(a.fix_counts + 4, 1);
-                    if (at < a.cap) a.flag[at] = make_int4(slot, row, (int)j, 0);
-                    else mx = fmaxf(mx, exact_dot<D>(qrow, krow[u], a.inv_scale_d));
+                const bool lst = j < lim && sub == 0 && hi >= floor_logit - fabsf(floor_logit) * 1e-6f;
+                // list it (the flag list is free once fix_flags ran; scored in parallel
+                // next) -- one counter atomic per warp: rows whose max ties across many
+                // keys (the generator's planted keys) list hundreds of them
+                const unsigned bal = __ballot_sync(kFull, lst);
+                if (bal) {
+                    int base = 0;
+                    if (lane == __ffs(bal) - 1) base = atomicAdd(a.fix_counts + 4, __popc(bal));
+                    base = __shfl_sync(kFull, base, __ffs(bal) - 1);
+                    if (lst) {
+                        const int at = base + __popc(bal & ((1u << lane) - 1u));
+                        if (at < a.cap) a.flag[at] = make_int4(slot, row, (int)j, 0);
+                        else mx = fmaxf(mx, exact_dot<D>(qrow, krow[u], a.inv_scale_d));
+                    }
                 }
             }
         }
@@ -197,11 +215,23 @@ __global__ void fix_rowmax(ScoreArgs a) {
     pdl_wait_then_release();
     const int n = min(a.fix_counts[4], a.cap);
     const int64_t R = (int64_t)a.G * a.w;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const int4 e = a.flag[i];
-        const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)e.x * R + e.y) * D);
-        const uint4* k = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) + ((int64_t)e.x * a.T + e.z) * D);
-        atomicMax(a.rmax_key + (int64_t)e.x * R + e.y, fkey(exact_dot<D>(q, k, a.inv_scale_d)));
+    const int stride = gridDim.x * blockDim.x;
+    const int n_up = (n + 31) / 32 * 32;   // warp-uniform trip count (the match below needs full warps)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_up; i += stride) {
+        const bool ok = i < n;
+        const int4 e = a.flag[ok ? i : 0];
+        unsigned key = 0u;
+        int64_t rr = -1;
+        if (ok) {
+            const uint4* q = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.q) + ((int64_t)e.x * R + e.y) * D);
+            const uint4* k = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(a.k) + ((int64_t)e.x * a.T + e.z) * D);
+            key = fkey(exact_dot<D>(q, k, a.inv_scale_d));
+            rr = (int64_t)e.x * R + e.y;
+        }
+        // lanes of the same row (listed consecutively) reduce first: one atomicMax per row and warp
+        const unsigned peers = __match_any_sync(kFull, (unsigned long long)rr);
+        const unsigned m = __reduce_max_sync(peers, key);
+        if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicMax(a.rmax_key + rr, m);
     }
 }
 
@@ -228,7 +258,7 @@ __global__ void fix_deferred(ScoreArgs a) {
 template <int D>
 cudaError_t launch_fixups(const ScoreArgs& a, cudaStream_t st) {
     cudaError_t e = launch_pdl(fix_flags<D>, dim3(592), dim3(256), 0, st, a);
-    if (e == cudaSuccess) e = launch_pdl(fix_rowscan<D>, dim3(24, 148), dim3(256), 0, st, a);
+    if (e == cudaSuccess) e = launch_pdl(fix_rowscan<D>, dim3(VLC_RS_X, VLC_RS_Y), dim3(256), 0, st, a);
     if (e == cudaSuccess) e = launch_pdl(fix_rowmax<D>, dim3(296), dim3(256), 0, st, a);
     if (e == cudaSuccess) e = launch_pdl(fix_deferred, dim3(148), dim3(256), 0, st, a);
     return e;
