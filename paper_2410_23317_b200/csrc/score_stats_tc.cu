@@ -447,9 +447,8 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
                         a.flag[at] = make_int4(s, (int)(r_first + rh), j, __float_as_int(minabs));
                         listed = true;
                         cntf = 0.f;
-                    } else {   // list full: keep the fp32 decisions (reported as overflow)
-                        atomicAdd(a.fix_counts + 2, 1);
-                        cntf += 0.f;   // entries in the band stay uncounted: the overflow raises
+                    } else {   // list full: the chunk's in-band entries stay undecided
+                        atomicAdd(a.fix_counts + 2, 1);   // (reported: check() raises ExactnessError)
                     }
                 }
             }

@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
     //    or the caller's float64 scores when scores_in is given (evict API)
     unsigned long long kmin = ~0ull, kmax = 0ull;
     const double group = (double)a.G;
+    const bool pow2 = (a.G & (a.G - 1)) == 0;
+    const double inv_group = 1.0 / group;
     // U keys per thread at a time with all their partial loads issued before
     // any is consumed (4 x U loads in flight instead of one dependent load at a
     // time); the partials still add in row-block order (fixed, position-free)
@@ -89,7 +91,8 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
                         if (rb0 + r < a.nrb) acc[u] = __dadd_rn(acc[u], (double)x[r][u]);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) sc[u] = __ddiv_rn(acc[u], group);
+            for (int u = 0; u < U; ++u)   // x / G == x * (1/G) exactly when G is a power of two
+                sc[u] = pow2 ? __dmul_rn(acc[u], inv_group) : __ddiv_rn(acc[u], group);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
