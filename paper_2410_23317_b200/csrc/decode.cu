@@ -58,6 +58,9 @@ constexpr int kStages = VLC_DEC_STAGES;
 #ifndef VLC_DEC_L2PF
 #define VLC_DEC_L2PF 0   // L2 bulk prefetch of the rows beyond the first ring (measured slower: 7.28 vs 7.12 us/step, B8 72.5 vs 66.6)
 #endif
+#ifndef VLC_DEC_EARLYLAUNCH
+#define VLC_DEC_EARLYLAUNCH 1
+#endif
 #ifndef VLC_DEC_PROBE
 #define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring, 4 = no wait for the previous step, 8 = no merge / output
 #endif
@@ -164,22 +167,32 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     // past its wait (this step's predecessor is then complete, so all the next
     // step reads early is final).  Without the guarantee (a.chained == 0)
     // everything waits up front.
+    // Early release (a.early: chained, and the step fills the GPU so at most about
+    // two steps are ever resident): the step releases its successor at once;
+    // since earlier steps may then still be running, every chunk holding rows
+    // they appended is loaded only after griddepcontrol.wait.  Otherwise the
+    // step releases its successor after that wait and only the chunk holding the
+    // previous step's append waits.
     const int pend = a.chained ? (int)((n - 2) / kChunk) : -1;
+    const bool early = a.chained && a.early;
+    const int first_dep = early ? (int)(a.base_len[s / a.Hkv] / kChunk) : pend;
+    auto deferred = [&](int c) { return c >= 0 && pend >= 0 && c >= first_dep && c <= pend; };
     bool waited = !a.chained;
     auto wait_prev = [&]() {
         if (!waited) {
             if (!(VLC_DEC_PROBE & 4)) asm volatile("griddepcontrol.wait;" ::: "memory");   // probe 4: no wait (racy)
-            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            if (!early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
             waited = true;
         }
     };
+    if (early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (!a.chained) {
         asm volatile("griddepcontrol.wait;" ::: "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     if (tid == 0) {
         for (int c = 0; c < kStages && c < nchunks; ++c)
-            if (c != pend) issue(c);
+            if (!deferred(c)) issue(c);
         // rows beyond the ring: start their HBM reads now (into L2), so the
         // refills that follow wait for L2, not HBM (a no-op when resident)
         if (VLC_DEC_L2PF && nchunks > kStages) {
@@ -205,9 +218,12 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             qb[kk][0] = qb[kk][1] = 0u;
         }
     }
-    if (tid == 0 && pend >= 0 && pend < kStages && pend < nchunks) {   // an initial chunk waits
-        wait_prev();
-        issue(pend);
+    if (tid == 0) {   // initial chunks that wait for the previous step
+        for (int c = 0; c < kStages && c < nchunks; ++c)
+            if (deferred(c)) {
+                wait_prev();
+                issue(c);
+            }
     }
     // O^T accumulators: tile t covers dims 16t..16t+15; c0,c1 = (dim 16t+row, heads 2q, 2q+1),
     // c2,c3 = (dim 16t+row+8, heads 2q, 2q+1)
@@ -245,7 +261,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
             if (lane == 0) sm100::mbar_arrive(&empty[st]);
             if (wig == 0 && lane == 0 && c + kStages < nchunks) {
                 sm100::mbar_wait(&empty[st], (c / kStages) & 1);
-                if (c + kStages == pend) wait_prev();
+                if (deferred(c + kStages)) wait_prev();
                 issue(c + kStages);
             }
             continue;
@@ -324,7 +340,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         if (lane == 0) sm100::mbar_arrive(&empty[st]);
         if (wig == 0 && lane == 0 && c + kStages < nchunks && !(VLC_DEC_PROBE & 2)) {
             sm100::mbar_wait(&empty[st], (c / kStages) & 1);
-            if (c + kStages == pend) wait_prev();             // holds the previous step's append
+            if (deferred(c + kStages)) wait_prev();           // holds rows earlier steps appended
             issue(c + kStages);
         }
     }
@@ -391,12 +407,17 @@ cudaError_t launch_dg(const DecodeArgs& a, const CUtensorMap& km, const CUtensor
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::kBytes;
     cfg.stream = st;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    DecodeArgs b = a;
+    b.early = (VLC_DEC_EARLYLAUNCH && a.slots >= n_sm) ? 1 : 0;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, decode_kernel<D, G>, km, vm, a);
+    return cudaLaunchKernelEx(&cfg, decode_kernel<D, G>, km, vm, b);
 }
 
 template <int D>

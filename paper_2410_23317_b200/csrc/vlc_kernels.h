@@ -137,6 +137,7 @@ struct DecodeArgs {
     float* out;                // f32 [B*L*Hq, d]
     int64_t cache_rows;        // rows of k_cache / v_cache (TMA bounds)
     int chained;               // the previous kernel on the stream is decode step `step - 1`
+    int early;                 // set by the launcher: release the successor at once (see decode.cu)
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
 
