@@ -63,7 +63,7 @@ constexpr int kAcc = VLC_K1_ACC;           // accumulator stages (a multiple of 
 static_assert(kAcc % kSets == 0 && kAcc * 128 <= 512, "accumulator stages");
 // registers: launch at 65536 / threads, then the control warpgroup drops to 32
 // and the epilogue warpgroups take the rest (setmaxnreg)
-constexpr int kRegLaunch = (65536 / (128 + kEpiWarps * 32)) & ~7;
+constexpr int kRegLaunch = (65536 / ((128 + kEpiWarps * 32) * VLC_K1_MINB)) & ~7;
 constexpr int kRegEpi = ((kRegLaunch * (128 + kEpiWarps * 32) - 128 * 32) / (kEpiWarps * 32)) & ~7;
 constexpr uint32_t kTmemCols = kAcc * kN <= 256 ? 256u : 512u;   // tcgen05.alloc: a power of two
 
