@@ -298,6 +298,26 @@ def test_exact_mode_margin_check():
         eng.check()
 
 
+@pytest.mark.parametrize("tau", [12, 40])
+def test_exact_mode_chunk_listing_straddling_heads(tau):
+    """Gaussian logits put many entries in exact mode's band; with windows of
+    12 / 40 rows a 32-row listing chunk spans two heads (the per-row head count
+    path).  Below counts per head still equal the oracle's exactly."""
+    rng = np.random.default_rng(7 + tau)
+    L, HQ, HKV, D, M = 2, 8, 2, 128, 700
+    q = bf16(rng.standard_normal((1, L, HQ, tau, D)) * 2.0)
+    k = bf16(rng.standard_normal((1, L, HKV, M, D)))
+    dq, dk = (torch.from_numpy(x).cuda().to(torch.bfloat16).contiguous() for x in (q, k))
+    eng = VLCache(Shape(1, L, HQ, HKV, D, M, tau))
+    eng.compress(dq, dk)
+    eng.check()
+    assert eng.exact_stats()["listed"] > 0
+    ref = O.compression_pass([q[0, l] for l in range(L)], [k[0, l] for l in range(L)], M, HQ // HKV)
+    ref_below = np.array([[ref["stats"][(l, h)][3].sum() for h in range(HQ)] for l in range(L)])
+    np.testing.assert_array_equal(eng.below_head.view(L, HQ).cpu().numpy(), ref_below)
+    np.testing.assert_array_equal(eng.kept_counts.cpu().numpy(), ref["kept_counts"])
+
+
 def test_decode_rejects_bad_inputs():
     """K5 does pointer arithmetic with the input shapes: non-contiguous views,
     wrong dtypes and mismatched K/V raise ValidationError before any launch."""
