@@ -54,6 +54,14 @@ def peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def m7b_config(batch, world):
+    """The bench line's config for the M7B workload (both arms print it)."""
+    return {"workload": "llava-1.6-mistral-7b shapes: L32 Hq32 Hkv8 d128 m2960 (16+2880+64) "
+                        "tau64 alpha0.1, 99 decode steps", "global_batch": batch * world,
+            "seq_len": CFG["prompt_len"], "parallelism": f"batch-sharded x{world} (no collective)",
+            "l2": "flushed (512 MB write) before every timed step"}
+
+
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` ("K1" / "K5") from the newest committed
     ncu --set full capture (profiles/r*_traffic.json, tools/ncu_traffic.py)."""
@@ -237,9 +245,8 @@ def run_reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (reference generator, bf16-rounded)",
-        "config": {"workload": "llava-1.6-mistral-7b shapes: L32 Hq32 Hkv8 d128 m2960 tau64 alpha0.1 "
-                               "batch1, 99 decode steps", "global_batch": 1, "seq_len": CFG["prompt_len"]},
+        "data": "synthetic (reference trace generator, bf16-rounded; seed = rank*B + b)",
+        "config": m7b_config(1, 1),   # the b200 arm's config at N = 1 (same workload)
         "compress_ms_per_prompt": tc * 1e3, "decode_tokens_per_s": (CFG["n_out"] - 1) / td,
         "cpu_baseline": {"value": value, "unit": "tok/s", **cpu_env(threads, kind),
                          "sample": cpu_sample_desc(threads), **extras},
@@ -479,10 +486,7 @@ def run_gpu_arm(args):
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (reference trace generator, bf16-rounded; seed = rank*B + b)",
-        "config": {"workload": "llava-1.6-mistral-7b shapes: L32 Hq32 Hkv8 d128 m2960 (16+2880+64) "
-                               "tau64 alpha0.1, 99 decode steps", "global_batch": B * world,
-                   "seq_len": c["prompt_len"], "parallelism": f"batch-sharded x{world} (no collective)",
-                   "l2": "flushed (512 MB write) before every timed step"},
+        "config": m7b_config(B, world),
         "compress_ms_per_prompt": (float(np.mean(k1)) + float(np.mean(k234))) / B,
         "k1_ms": k1_ms, "k234_ms": float(np.mean(k234)), "decode_ms_99_steps": dec_ms,
         "decode_tokens_per_s": B * n_dec * world / (dec_ms / 1e3),
