@@ -501,6 +501,8 @@ def run_gpu_arm(args):
         "gpu_launches": args.steps * (9 + n_dec),   # zeroing, K1, 4 exact fix-ups, K2, K3, K4, 99 x K5
         "clocks": clk.summary(),
         "kept_tokens_per_layer_mean": float(counts.mean()),
+        # exact mode's counters of the last timed compress and its runtime margin check
+        "exact_mode": eng.exact_stats(),
     }
     line["k1_mufu"]["frac"] = line["k1_mufu"]["floor_us"] / (k1_ms * 1e3)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
