@@ -9,8 +9,10 @@
 // One CTA per slot.  Each float64 score maps to an order-preserving uint64
 // key (sign-flip trick; -0.0 folded onto +0.0 so equal values tie as numpy
 // sees them); an MSB-first 8-bit radix select finds the exact k-th key T;
-// ties at T are resolved toward larger indices by a right-to-left rank; a
-// block scan compacts the kept flags in index order.
+// a bucket whose keys are all equal (a run of ties, common with planted
+// duplicate keys) ends the passes at once; ties at T are resolved toward larger
+// indices by a right-to-left rank; warp ballots + a prefix over the per-warp
+// counts (register path) or a block scan compact the kept flags in index order.
 #include "vlc_common.cuh"
 #include "vlc_kernels.h"
 
@@ -38,6 +40,7 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
     __shared__ unsigned long long s_prefix, s_mask;
     __shared__ long long s_want;
     __shared__ unsigned long long s_min, s_max;
+    __shared__ unsigned long long s_bmin, s_bmax;   // current bucket's extremes
     __shared__ int s_small;                        // bucket small enough for the warp finish
     __shared__ unsigned long long s_cand[32];      // its keys
     __shared__ int s_ncand;
@@ -106,6 +109,10 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
         }
     }
     __syncthreads();
+#ifdef VLC_K3_PROBE    // timing probe (wrong results): phase 1 only -- scores and keys
+    if (tid == 0 && kmin == 12345ull) a.kept_idx[0] = 0;
+    return;
+#endif
     if (tid == 0) { s_min = ~0ull; s_max = 0ull; s_prefix = 0ull; s_mask = 0ull; s_want = nk; s_small = 0; s_ncand = 0; }
     __syncthreads();
 #pragma unroll
@@ -134,14 +141,17 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
         for (int pass = top_pass; pass >= 0; --pass) {
             const int shift = pass * 8;
             for (int i = tid; i < 256; i += kThreads) hist[i] = 0;
+            if (tid == 0) { s_bmin = ~0ull; s_bmax = 0ull; }
             __syncthreads();
             const unsigned long long prefix = s_prefix, mask = s_mask;
+            unsigned long long bmin = ~0ull, bmax = 0ull;   // the bucket's extremes
             if (RK > 0) {
 #pragma unroll
                 for (int u = 0; u < (RK > 0 ? RK : 1); ++u) {
                     const int64_t j = tid + (int64_t)u * kThreads;
                     const bool in = j < ncand && ((kreg[u] & mask) == prefix);
                     if (!__any_sync(kFull, in)) continue;   // warp-uniform
+                    if (in) { bmin = min(bmin, kreg[u]); bmax = max(bmax, kreg[u]); }
                     const unsigned dgt = in ? (unsigned)((kreg[u] >> shift) & 255u) : 256u;
                     const unsigned peers = __match_any_sync(kFull, dgt);
                     if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
@@ -151,12 +161,26 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
                     const int64_t j = j0 + tid;
                     const bool in = j < ncand && ((keys[j] & mask) == prefix);
                     if (!__any_sync(kFull, in)) continue;   // warp-uniform
+                    if (in) { bmin = min(bmin, keys[j]); bmax = max(bmax, keys[j]); }
                     const unsigned dgt = in ? (unsigned)((keys[j] >> shift) & 255u) : 256u;
                     const unsigned peers = __match_any_sync(kFull, dgt);
                     if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[dgt], __popc(peers));
                 }
             }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                bmin = min(bmin, __shfl_xor_sync(kFull, bmin, o));
+                bmax = max(bmax, __shfl_xor_sync(kFull, bmax, o));
+            }
+            if (lane == 0 && bmin <= bmax) { atomicMin(&s_bmin, bmin); atomicMax(&s_bmax, bmax); }
             __syncthreads();
+            if (s_bmin == s_bmax) {
+                // one distinct key left in the bucket (a run of ties): it is T and
+                // the remaining want are ties at T -- no further passes
+                if (tid == 0) s_prefix = s_bmin;
+                __syncthreads();
+                break;
+            }
             if (warp == 0) {
                 // lane L covers digits 255-8L .. 248-8L (descending)
                 unsigned c[8];
@@ -227,8 +251,83 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
             __syncthreads();
         }
     }
+#ifdef VLC_K3_PROBE2   // timing probe (wrong results): phases 1-2 -- no emission
+    if (tid == 0 && s_prefix == 12345ull) a.kept_idx[0] = 0;
+    return;
+#endif
     const unsigned long long T = s_prefix;
     const long long need = s_want;   // ties at T to keep (largest indices first)
+
+    if (RK > 0) {
+        // 3'. keys in registers: j = tid + u*kThreads orders as (u, warp, lane),
+        //     so warp ballots + one prefix over the (u, warp) counts give each
+        //     tie its rank from the right and each kept key its output slot
+        constexpr int W = kThreads / 32, E = (RK > 0 ? RK : 2) * W / 32;
+        static_assert(RK == 0 || (RK * W) % 32 == 0, "prefix layout");
+        __shared__ int s_cnt[RK > 0 ? RK * W : 1], s_pre[RK > 0 ? RK * W : 1], s_tot;
+        auto prefix_counts = [&]() {   // s_pre = exclusive prefix of s_cnt, s_tot = sum (warp 0)
+            if (warp == 0) {
+                int c[E], t = 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) { c[e] = s_cnt[lane * E + e]; t += c[e]; }
+                int incl = t;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int run = incl - t;
+#pragma unroll
+                for (int e = 0; e < E; ++e) { s_pre[lane * E + e] = run; run += c[e]; }
+                if (lane == 31) s_tot = incl;
+            }
+        };
+        const unsigned below = (1u << lane) - 1u;
+        unsigned tb[RK > 0 ? RK : 1];
+#pragma unroll
+        for (int u = 0; u < (RK > 0 ? RK : 1); ++u) {
+            const int64_t j = tid + (int64_t)u * kThreads;
+            tb[u] = __ballot_sync(kFull, nk > 0 && j < ncand && kreg[u] == T);
+            if (lane == 0) s_cnt[u * W + warp] = __popc(tb[u]);
+        }
+        __syncthreads();
+        prefix_counts();
+        __syncthreads();
+        const int ties_total = s_tot;
+        unsigned kb[RK > 0 ? RK : 1];
+#pragma unroll
+        for (int u = 0; u < (RK > 0 ? RK : 1); ++u) {
+            const int64_t j = tid + (int64_t)u * kThreads;
+            bool keep = false;
+            if (j < n) {
+                if (j >= ncand) keep = true;
+                else if (nk > 0) {
+                    if (kreg[u] > T) keep = true;
+                    else if ((tb[u] >> lane) & 1u) {   // ties strictly to the right
+                        const int right = ties_total - (s_pre[u * W + warp] + __popc(tb[u] & below)) - 1;
+                        keep = right < need;
+                    }
+                }
+            }
+            kb[u] = __ballot_sync(kFull, keep);
+        }
+        __syncthreads();   // every thread has read s_pre / s_tot
+#pragma unroll
+        for (int u = 0; u < (RK > 0 ? RK : 1); ++u)
+            if (lane == 0) s_cnt[u * W + warp] = __popc(kb[u]);
+        __syncthreads();
+        prefix_counts();
+        __syncthreads();
+        const int64_t base = a.kept_off[s];
+#pragma unroll
+        for (int u = 0; u < (RK > 0 ? RK : 1); ++u)
+            if ((kb[u] >> lane) & 1u) {
+                const int64_t pos = base + s_pre[u * W + warp] + __popc(kb[u] & below);
+                a.kept_idx[pos] = (int32_t)(tid + u * kThreads);
+                a.kept_slot[pos] = s;
+            }
+        return;
+    }
 
     // 3. chunked flags in index order.  A tie at T is kept iff fewer than
     //    `need` ties lie strictly to its right (ties toward the larger index).

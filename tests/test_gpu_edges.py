@@ -64,6 +64,22 @@ def test_long_score_rows_use_global_scratch():
             np.testing.assert_array_equal(vl.evict(s, k, vl.EvictionConfig(frac)), O.evict(s, k, frac))
 
 
+def test_register_path_tie_runs_and_ragged_sizes():
+    """n <= 3072 keeps keys in registers: runs of > 32 equal scores at the
+    k-th position (the uniform-bucket exit), sizes off the 512-thread grid,
+    k = 1 / n, and a reserve covering the whole budget (no key chosen by score)."""
+    import paper_2410_23317_b200 as vl
+
+    rng = np.random.default_rng(5)
+    for n in (1, 31, 512, 513, 1999, 2960, 3072):
+        for vals in (3, 40, 0):
+            s = rng.integers(0, vals, n).astype(np.float64) if vals else rng.standard_normal(n)
+            for k in sorted({1, n // 3, n // 2, n - 1, n} - {0}):   # the API rejects k = 0
+                for frac in (0.0, 0.1, 1.0):
+                    np.testing.assert_array_equal(vl.evict(s, k, vl.EvictionConfig(frac)), O.evict(s, k, frac),
+                                                  err_msg=f"n={n} vals={vals} k={k} frac={frac}")
+
+
 def test_negative_and_signed_zero_scores():
     import paper_2410_23317_b200 as vl
 
