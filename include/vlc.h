@@ -152,6 +152,19 @@ VLC_API int vlc_select(const float *col_partial, const double *scores_in, int32_
                void *stream);
 
 /*
+ * vlc_select for a launch that directly follows vlc_allocate /
+ * vlc_allocate_from_gamma on the same stream, with col_partial written before
+ * that allocation (the engine's compress order K1 -> K2 -> K3).  Same
+ * arguments and results; K3 sums and ranks the scores while K2 still runs and
+ * waits for K2 only to read the budgets.  scores_in must be NULL.
+ */
+VLC_API int vlc_select_after_allocate(const float *col_partial, const double *scores_in, int32_t slots,
+               int32_t kv_heads, int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+               const int64_t *kept_counts, const int64_t *kept_off, double recent_frac,
+               int32_t *kept_idx, int32_t *kept_slot, double *scores_out, uint64_t *key_scratch,
+               void *stream);
+
+/*
  * K4 gather.  Copies keys/values[s, kept_idx] into the cache segment of slot s
  * (reference bench.py:331-353).  max_rows: host upper bound on sum of kept
  * counts (sizes the grid; the device total is kept_off[slots]).

@@ -40,6 +40,8 @@ _SIGNATURES = {
                                                _P, _P, _P, _P, _P, _P, _P]),
     "vlc_select": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I64, _I64, _P, _P, _F64, _P, _P,
                                   _P, _P, _P]),
+    "vlc_select_after_allocate": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I64, _I64, _P, _P, _F64, _P,
+                                                 _P, _P, _P, _P]),
     "vlc_gather": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _I64, _P, _P, _P]),
     "vlc_copy_2d": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "vlc_decode_step": (ctypes.c_int, [_P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _I32,

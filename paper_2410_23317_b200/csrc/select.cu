@@ -33,7 +33,12 @@ __device__ __forceinline__ unsigned long long order_key(double x) {
 // loads at once; RK == 0: any n, keys re-read from shared / global memory.
 template <int RK>
 __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
-    pdl_wait_then_release();
+    // scores_ready (vlc_select_after_allocate): col_partial was final before the
+    // preceding K2 released this grid, so phase 1 runs under K2 and only the
+    // budgets wait; its loads bypass L1 (ld.global.cg) since this grid has not
+    // passed a dependency wait yet
+    const bool early = a.scores_ready && !a.scores_in;
+    if (!early) pdl_wait_then_release();
     extern __shared__ unsigned long long keys_smem[];
     __shared__ unsigned int hist[256];
     __shared__ long long scan_scratch[32];
@@ -48,10 +53,6 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s = blockIdx.x;
     const int64_t n = a.n;
-    const int64_t k = a.kept_counts[s / a.Hkv];  // same budget for every KV head of a layer
-    const int64_t reserve = imin((int64_t)ceil(a.recent_frac * (double)k), k);
-    const int64_t nk = k - reserve;
-    const int64_t ncand = n - reserve;
     unsigned long long* keys = (n <= kSmemKeysMax) ? keys_smem : a.key_scratch + (int64_t)s * n;
 
     // 1. score = (sum over row blocks, fixed order, fp64) / G  (scoring.py:198-201),
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int64_t j = j0 + (int64_t)u * kThreads;
-                        x[r][u] = (rb0 + r < a.nrb && j < n) ? cp[(int64_t)(rb0 + r) * n + j] : 0.f;
+                        x[r][u] = (rb0 + r < a.nrb && j < n) ? __ldcg(cp + (int64_t)(rb0 + r) * n + j) : 0.f;
                     }
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
@@ -103,10 +104,20 @@ __global__ void __launch_bounds__(kThreads, 2) select_kernel(SelectArgs a) {
             if (RK > 0) kreg[RK > 0 ? u : 0] = order_key(sc[u]);
             if (j >= n) continue;
             if (!a.scores_in && a.scores) a.scores[(int64_t)s * n + j] = sc[u];
-            const unsigned long long key = order_key(sc[u]);
-            keys[j] = key;
-            if (j < ncand) { kmin = min(kmin, key); kmax = max(kmax, key); }
+            keys[j] = order_key(sc[u]);
         }
+    }
+    if (early) pdl_wait_then_release();   // K2 done: the budgets are final
+    const int64_t k = a.kept_counts[s / a.Hkv];  // same budget for every KV head of a layer
+    const int64_t reserve = imin((int64_t)ceil(a.recent_frac * (double)k), k);
+    const int64_t nk = k - reserve;
+    const int64_t ncand = n - reserve;
+    if (RK > 0) {
+#pragma unroll
+        for (int u = 0; u < (RK > 0 ? RK : 1); ++u)
+            if (tid + (int64_t)u * kThreads < ncand) { kmin = min(kmin, kreg[u]); kmax = max(kmax, kreg[u]); }
+    } else {
+        for (int64_t j = tid; j < ncand; j += kThreads) { kmin = min(kmin, keys[j]); kmax = max(kmax, keys[j]); }
     }
     __syncthreads();
 #ifdef VLC_K3_PROBE    // timing probe (wrong results): phase 1 only -- scores and keys

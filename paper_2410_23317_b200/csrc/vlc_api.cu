@@ -211,11 +211,11 @@ int vlc_allocate_from_gamma(const double* gamma_mean, int32_t batch, int32_t lay
     return cuda_status(vlc::launch_allocate(a, (cudaStream_t)stream), "allocate");
 }
 
-int vlc_select(const float* col_partial, const double* scores_in, int32_t slots, int32_t kv_heads,
-               int32_t layers, int32_t group, int64_t n_keys, int64_t window,
-               const int64_t* kept_counts, const int64_t* kept_off, double recent_frac,
-               int32_t* kept_idx, int32_t* kept_slot, double* scores_out, uint64_t* key_scratch,
-               void* stream) {
+static int select_impl(const float* col_partial, const double* scores_in, int32_t slots, int32_t kv_heads,
+                       int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+                       const int64_t* kept_counts, const int64_t* kept_off, double recent_frac,
+                       int32_t* kept_idx, int32_t* kept_slot, double* scores_out, uint64_t* key_scratch,
+                       void* stream, int scores_ready) {
     if ((!col_partial && !scores_in) || !kept_counts || !kept_off || !kept_idx || !kept_slot)
         return fail(VLC_EINVAL, "select: null pointer");
     if (slots < 1 || kv_heads < 1 || layers < 1 || group < 1 || n_keys < 1 || window < 1)
@@ -233,7 +233,29 @@ int vlc_select(const float* col_partial, const double* scores_in, int32_t slots,
     a.kept_counts = kept_counts; a.kept_off = kept_off; a.recent_frac = recent_frac;
     a.kept_idx = kept_idx; a.kept_slot = kept_slot; a.scores = scores_out; a.scores_in = scores_in;
     a.key_scratch = reinterpret_cast<unsigned long long*>(key_scratch);
+    a.scores_ready = scores_ready;
     return cuda_status(vlc::launch_select(a, (cudaStream_t)stream), "select");
+}
+
+int vlc_select(const float* col_partial, const double* scores_in, int32_t slots, int32_t kv_heads,
+               int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+               const int64_t* kept_counts, const int64_t* kept_off, double recent_frac,
+               int32_t* kept_idx, int32_t* kept_slot, double* scores_out, uint64_t* key_scratch,
+               void* stream) {
+    return select_impl(col_partial, scores_in, slots, kv_heads, layers, group, n_keys, window, kept_counts,
+                       kept_off, recent_frac, kept_idx, kept_slot, scores_out, key_scratch, stream, 0);
+}
+
+// K2 waits for every earlier kernel before it releases K3 (pdl_wait_then_release),
+// so col_partial is final when K3 launches: K3 reads it before its own wait
+int vlc_select_after_allocate(const float* col_partial, const double* scores_in, int32_t slots,
+                              int32_t kv_heads, int32_t layers, int32_t group, int64_t n_keys, int64_t window,
+                              const int64_t* kept_counts, const int64_t* kept_off, double recent_frac,
+                              int32_t* kept_idx, int32_t* kept_slot, double* scores_out, uint64_t* key_scratch,
+                              void* stream) {
+    if (scores_in) return fail(VLC_EINVAL, "select_after_allocate: scores_in must be NULL");
+    return select_impl(col_partial, scores_in, slots, kv_heads, layers, group, n_keys, window, kept_counts,
+                       kept_off, recent_frac, kept_idx, kept_slot, scores_out, key_scratch, stream, 1);
 }
 
 int vlc_gather(const void* keys, const void* values, int32_t slots, int32_t head_dim,

@@ -101,6 +101,7 @@ struct SelectArgs {
     double* scores;            // optional out [slots, n]
     const double* scores_in;   // optional in [slots, n]: rank these instead of col_partial
     unsigned long long* key_scratch;  // [slots, n] when n > 24576
+    int scores_ready;          // col_partial final at launch (K2 precedes): sum before the PDL wait
 };
 cudaError_t launch_select(const SelectArgs& a, cudaStream_t st);
 

@@ -135,6 +135,7 @@ class VLCache:
         self.kept_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
         self.cache_off = torch.empty(s.slots + 1, dtype=i64, device=dev)
         self.status = torch.zeros(s.B, dtype=i32, device=dev)
+        self._alloc_last = False   # the last launch on the path was K2 (see select)
         self.max_rows = kept_rows_bound(s.B, s.L, s.Hkv, s.m, alpha, beta_min)
         self.kept_idx = torch.empty(self.max_rows, dtype=i32, device=dev)
         self.kept_slot = torch.empty(self.max_rows, dtype=i32, device=dev)
@@ -178,6 +179,7 @@ class VLCache:
         """K1 over all slots; fills row_max/row_sum/col_partial/below_head."""
         s = self.shape
         self._check_inputs(q_win, keys)
+        self._alloc_last = False   # col_partial is being rewritten
         _lib.call("vlc_score_stats", q_win.data_ptr(), keys.data_ptr(), s.slots, s.G, s.d,
                   keys.shape[3], s.m, s.w, s.m - s.w, self.p, self.scale, _ptr(self.row_max), _ptr(self.row_sum),
                   _ptr(self.col_partial), _ptr(self.below_head), _ptr(below_col), _ptr(self.exact_ws),
@@ -186,6 +188,7 @@ class VLCache:
     def allocate(self):
         """K2 from the below-threshold counts currently in below_head."""
         s = self.shape
+        self._alloc_last = True   # the next select() may rank under this launch
         _lib.call("vlc_allocate", _ptr(self.below_alloc), s.B, s.L, self.hq_alloc, s.Hkv, s.w, s.m, s.m - s.w,
                   s.m, self.alpha, self.beta_min, self.beta_max, self.decode_steps, _ptr(self.gamma),
                   _ptr(self.gamma_mean), _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
@@ -202,13 +205,18 @@ class VLCache:
         if tuple(gamma_mean.shape) != (s.B, s.L) or gamma_mean.dtype != torch.float64 or not gamma_mean.is_cuda:
             raise ValidationError(f"gamma_mean: expected a float64 CUDA tensor [{s.B}, {s.L}]")
         self.gamma_mean.copy_(gamma_mean.reshape(-1))
+        self._alloc_last = True   # the next select() may rank under this launch
         _lib.call("vlc_allocate_from_gamma", _ptr(self.gamma_mean), s.B, s.L, s.Hkv, s.m, self.alpha, self.beta_min,
                   self.beta_max, self.decode_steps, _ptr(self.beta_pre), _ptr(self.beta), _ptr(self.kept_counts),
                   _ptr(self.kept_off), _ptr(self.cache_off), _ptr(self.status), _stream())
 
     def select(self):
+        """K3.  Directly after allocate() (and with col_partial written before it)
+        K3 sums the scores while K2 runs (vlc_select_after_allocate)."""
         s = self.shape
-        _lib.call("vlc_select", _ptr(self.col_partial), 0, s.slots, s.Hkv, s.L, s.G, s.m, s.w,
+        fn = "vlc_select_after_allocate" if self._alloc_last else "vlc_select"
+        self._alloc_last = False
+        _lib.call(fn, _ptr(self.col_partial), 0, s.slots, s.Hkv, s.L, s.G, s.m, s.w,
                   _ptr(self.kept_counts), _ptr(self.kept_off), self.recent_frac, _ptr(self.kept_idx),
                   _ptr(self.kept_slot), _ptr(self.scores), _ptr(self.key_scratch), _stream())
 
@@ -243,6 +251,7 @@ class VLCache:
         self._check_inputs(q_win, keys)
         if tuple(stat_max.shape[-1:]) != (s.m,) or stat_max.numel() != s.B * s.L * s.Hq * s.m:
             raise ValidationError(f"stat_max: expected [B, L, Hq, {s.m}] prefill statistics")
+        self._alloc_last = False   # col_partial is being rewritten
         _lib.call("vlc_score_stats_given", q_win.data_ptr(), keys.data_ptr(), s.slots, s.G, s.d,
                   keys.shape[3], s.m, s.w, s.m - s.w, self.p, self.scale, stat_max.data_ptr(), stat_sum.data_ptr(),
                   s.m, _ptr(self.row_max), _ptr(self.row_sum), _ptr(self.col_partial), _ptr(self.below_head), 0,
@@ -373,6 +382,7 @@ class VLCache:
         slot0 = (b * s.L + l0) * s.Hkv
         R, esz = s.G * s.w, 2
         T = keys.shape[3]
+        self._alloc_last = False   # col_partial is being rewritten
         _lib.call("vlc_score_stats", q_win.data_ptr() + slot0 * R * s.d * esz, keys.data_ptr() + slot0 * T * s.d * esz,
                   (l1 - l0) * s.Hkv, s.G, s.d, T, s.m, s.w, s.m - s.w, self.p, self.scale,
                   _ptr(self.row_max) + slot0 * R * 4, _ptr(self.row_sum) + slot0 * R * 4,

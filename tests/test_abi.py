@@ -61,6 +61,8 @@ def test_contract_errors_map_to_reference_types():
     assert rc == _lib.VLC_EINVAL and b"alpha" in lib.vlc_last_error()
     rc = lib.vlc_select(d, None, 4, 2, 2, 1, 10, 2, d, d, 1.5, d, d, None, None, None)
     assert rc == _lib.VLC_EINVAL and b"recent_window_frac" in lib.vlc_last_error()
+    rc = lib.vlc_select_after_allocate(d, d, 4, 2, 2, 1, 10, 2, d, d, 0.1, d, d, None, None, None)
+    assert rc == _lib.VLC_EINVAL and b"scores_in" in lib.vlc_last_error()
     rc = lib.vlc_decode_step(d, 64, d, d, 64, d, d, 10, d, d, 0, 1, 1, 1, 9, 64, 0.0, 0, d, None)
     assert rc == _lib.VLC_EUNSUPPORTED
     rc = lib.vlc_score_stats(d, d, 1, 1, 48, 10, 10, 2, 8, 0.01, 0.0, d, d, d, d, None, None, 0, None)
