@@ -5,14 +5,15 @@
 // KV head) and _core.pyx:245-278 (decode_step: softmax(q K^T / sqrt(d)) V, fp32).
 //
 // One CTA per (b, l, kv) slot streams the slot's K and V rows through a
-// 6-stage shared-memory ring of 32-row chunks, loaded by 2-D TMA with the
+// 6-stage shared-memory ring of 16-row chunks, loaded by 2-D TMA with the
 // 128-byte swizzle so tensor-core fragments come out of shared memory
-// conflict-free.  Four groups of two warps take chunks round robin (group
-// c % 4 consumes chunk c), so four chunks are in compute at once and the
-// serial chain of the slot's longest-budget layers is a quarter; inside a
-// group warp w owns rows 16w .. 16w+15 of the chunk.  (Round 1 used two
-// groups of four warps on 64-row chunks in a 3-stage ring: 6.68 vs 6.61
-// us/step at M7B, 63.4 vs 62.2 at batch 8.)  The G <= 8 query heads of the KV head
+// conflict-free.  Four one-warp groups take chunks round robin (group c % 4
+// consumes chunk c), so four chunks are in compute at once and the serial
+// chain of the slot's longest-budget layers is a quarter.  A CTA is 128
+// threads and 48 KB of ring, so four fit per SM: two steps' grids (256 CTAs
+// each at M7B) are resident together and the next step's prologue, loads and
+// base-row chunks run under the current one (5.5 vs 6.2 us/step for two
+// two-warp groups per chunk at 96 KB, 56 vs 62 at batch 8).  The G <= 8 query heads of the KV head
 // are the N = 8 columns of transposed mma.sync tiles (GQA: every key row is
 // read from HBM once per step for the whole group; no padding of the big M side):
 //   S^T = K Q^T    m16n8k16, M = 16 keys, bf16 in, fp32 accumulate (exact products);
@@ -25,10 +26,11 @@
 // for the previous step: everything else is loaded and computed while it
 // drains.  Each stage has two full barriers used alternately, so a group that
 // runs a ring ahead of another never mistakes a stage's previous use for its
-// chunk.  A stage is refilled as soon as the four
-// warps that consumed it arrive on its "empty" barrier.  The chunk holding row
-// k + step takes it from k_new / v_new (patched into the swizzled tile) and
-// also appends it to the cache for later steps.
+// chunk.  A stage is refilled as soon as the warps that consumed it arrive on
+// its "empty" barrier.  The chunk holding row k + step takes that row from
+// k_new / v_new through a small swizzled side buffer (the lanes whose ldmatrix
+// row it is read there; the ring is only ever written by TMA) and appends it
+// to the cache for later steps.
 #include "sm100.cuh"
 #include "vlc_common.cuh"
 #include "vlc_kernels.h"
@@ -37,7 +39,7 @@ namespace vlc {
 namespace {
 
 #ifndef VLC_DEC_GROUP_WARPS
-#define VLC_DEC_GROUP_WARPS 2
+#define VLC_DEC_GROUP_WARPS 1
 #endif
 #ifndef VLC_DEC_GROUPS
 #define VLC_DEC_GROUPS 4
@@ -60,6 +62,9 @@ constexpr int kStages = VLC_DEC_STAGES;
 #endif
 #ifndef VLC_DEC_EARLYLAUNCH
 #define VLC_DEC_EARLYLAUNCH 1
+#endif
+#ifndef VLC_DEC_EARLY_PERIOD
+#define VLC_DEC_EARLY_PERIOD 16   // under early release, every P-th step releases late (bounds the deferred rows)
 #endif
 #ifndef VLC_DEC_PROBE
 #define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring, 4 = no wait for the previous step, 8 = no merge / output
@@ -124,6 +129,12 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     // for its chunk's (a parity wait alone would accept the previous use)
     __shared__ uint64_t bar[kStages][2], empty[kStages];
     __shared__ float part_m[kWarps][8], part_s[kWarps][8];
+    // the step's new K / V row (one chunk per CTA holds it), laid out like its
+    // row of a swizzled tile with the row term dropped: the lanes whose
+    // ldmatrix row is the new row take this as their row base, so the TMA ring
+    // is never written by threads
+    constexpr uint32_t kNewBytes = (Cfg<D>::KB - 1) * Cfg<D>::kBox + 128;
+    __shared__ __align__(128) uint8_t new_kv[2][kNewBytes];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int grp = warp / kGroupWarps, wig = warp % kGroupWarps;   // consumer group, warp in group
@@ -174,8 +185,15 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
     // step releases its successor after that wait and only the chunk holding the
     // previous step's append waits.
     const int pend = a.chained ? (int)((n - 2) / kChunk) : -1;
-    const bool early = a.chained && a.early;
-    const int first_dep = early ? (int)(a.base_len[s / a.Hkv] / kChunk) : pend;
+    constexpr int kPeriod = VLC_DEC_EARLY_PERIOD;
+    const bool early = a.chained && a.early && (a.step % kPeriod) != 0;   // this step releases at once
+    // rows whose appends may still be in flight: those of steps t .. step-1, t the
+    // latest step that released late (it had waited, so every step before t is complete)
+    int first_dep = pend;
+    if (a.chained && a.early) {
+        const int64_t prev = a.step - 1, t = prev - prev % kPeriod;
+        first_dep = (int)((a.base_len[s / a.Hkv] + t) / kChunk);
+    }
     auto deferred = [&](int c) { return c >= 0 && pend >= 0 && c >= first_dep && c <= pend; };
     bool waited = !a.chained;
     auto wait_prev = [&]() {
@@ -241,20 +259,21 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         // chunk c is use c / kStages of its stage: wait on that use's barrier
         if (!((VLC_DEC_PROBE & 2) && c >= kStages))
             sm100::mbar_wait(&bar[st][(c / kStages) & 1], (c / (2 * kStages)) & 1);
-        if (new_row < j0 + kChunk) {   // last chunk: patch in the new row (group-uniform)
+        const bool has_new = new_row < j0 + kChunk;   // last chunk (group-uniform)
+        if (has_new) {   // the new row: into this group's row buffer and appended to the cache
             wait_prev();                                           // the append is a global write
-            const int r = (int)(new_row - j0);
-            const int gt = tid % (kGroupWarps * 32);
-            if (gt < 2 * (D / 8)) {
+            for (int gt = tid % (kGroupWarps * 32); gt < 2 * (D / 8); gt += kGroupWarps * 32) {
                 const bool isv = gt >= D / 8;
                 const int piece = gt % (D / 8);
                 const uint4 val = reinterpret_cast<const uint4*>(
                     static_cast<const __nv_bfloat16*>(isv ? a.v_new : a.k_new) + (int64_t)s * a.kv_stride)[piece];
-                *reinterpret_cast<uint4*>((isv ? vs : ks) + swz<D>(r, piece)) = val;
+                *reinterpret_cast<uint4*>(new_kv[isv] + (piece >> 3) * C::kBox +
+                                          (((piece & 7) ^ (int)((new_row - j0) & 7)) << 4)) = val;
                 reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(isv ? a.v_cache : a.k_cache) +
                                          (seg + new_row) * D)[piece] = val;
             }
-            sm100::named_bar_sync(1 + grp, kGroupWarps * 32);
+            if (kGroupWarps == 1) __syncwarp();   // a one-warp group: the warp's own barrier
+            else sm100::named_bar_sync(1 + grp, kGroupWarps * 32);
         }
         if (VLC_DEC_PROBE & 1) {   // timing probe: no math
             __syncwarp();
@@ -271,14 +290,16 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         float sacc[4] = {0.f, 0.f, 0.f, 0.f};
         const uint32_t kbase = sm100::smem_u32(ks);
         const int arow = kr + (lane & 7) + ((lane >> 3) & 1) * 8;   // ldmatrix row of this lane
+        const uint32_t krow = (has_new && j0 + arow == new_row) ? sm100::smem_u32(new_kv[0]) : kbase + arow * 128;
+        auto kaddr = [&](int piece) { return krow + swz<D>(arow, piece) - arow * 128; };
 #if VLC_DEC_SCHAINS == 2
         // two independent accumulator chains over the k-steps (half the HMMA latency chain)
         float sacc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int kk = 0; kk < D / 16; kk += 2) {
             uint32_t af[4], ag[4];
-            ldsm_x4(kbase + swz<D>(arow, kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
-            ldsm_x4(kbase + swz<D>(arow, (kk + 1) * 2 + (lane >> 4)), ag[0], ag[1], ag[2], ag[3]);
+            ldsm_x4(kaddr(kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
+            ldsm_x4(kaddr((kk + 1) * 2 + (lane >> 4)), ag[0], ag[1], ag[2], ag[3]);
             mma16(sacc, af, qb[kk][0], qb[kk][1]);
             mma16(sacc2, ag, qb[kk + 1][0], qb[kk + 1][1]);
         }
@@ -288,7 +309,7 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
             uint32_t af[4];
-            ldsm_x4(kbase + swz<D>(arow, kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
+            ldsm_x4(kaddr(kk * 2 + (lane >> 4)), af[0], af[1], af[2], af[3]);
             mma16(sacc, af, qb[kk][0], qb[kk][1]);
         }
 #endif
@@ -328,10 +349,12 @@ decode_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ 
         // ---- O^T += V^T P^T: V^T A fragments by transposed ldmatrix of the warp's 16 rows
         const uint32_t vbase = sm100::smem_u32(vs);
         const int vrow = kr + (lane & 7) + (lane >> 4) * 8;
+        const uint32_t vrowb = (has_new && j0 + vrow == new_row) ? sm100::smem_u32(new_kv[1]) : vbase + vrow * 128;
 #pragma unroll
         for (int t = 0; t < C::MT; ++t) {
             uint32_t af[4];
-            ldsm_x4_t(vbase + swz<D>(vrow, t * 2 + ((lane >> 3) & 1)), af[0], af[1], af[2], af[3]);
+            const int piece = t * 2 + ((lane >> 3) & 1);
+            ldsm_x4_t(vrowb + swz<D>(vrow, piece) - vrow * 128, af[0], af[1], af[2], af[3]);
             mma16(o[t], af, bh0, bh1);
             mma16(o[t], af, bl0, bl1);
         }

@@ -16,7 +16,7 @@ from paper_2410_23317_b200.trace import GenSpec, device_synthetic  # noqa: E402
 # SAN_L / SAN_HKV: enough (layer, KV head) slots (>= the SM count) to take K5's
 # early-release path as well
 L, HKV = int(os.environ.get("SAN_L", "2")), int(os.environ.get("SAN_HKV", "2"))
-HQ, D, M, TAU, N = 4 * HKV, 128, 624, 32, 3
+HQ, D, M, TAU, N = 4 * HKV, 128, 624, 32, int(os.environ.get("SAN_N", "3"))   # SAN_N > 16: K5's periodic late release
 spec = GenSpec(num_layers=L, num_query_heads=HQ, num_kv_heads=HKV, head_dim=D, prompt_len=M, post_vision_len=TAU,
                decode_len=N, seed=0)
 qw, qd, k, v = device_synthetic(spec, 1, TAU)
