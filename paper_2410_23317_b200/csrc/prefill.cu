@@ -96,8 +96,8 @@ prefill_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
     [[maybe_unused]] float2* rowstat = reinterpret_cast<float2*>(sp);   // [4 * kM], pass 1 only (P is pass 2 only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sq_slot = blockIdx.y;                                  // (b, l, query head)
-    const int rb = gridDim.x - 1 - blockIdx.x;                       // longest blocks first
+    const int sq_slot = blockIdx.x;                                  // (b, l, query head)
+    const int rb = gridDim.y - 1 - blockIdx.y;                       // longest blocks first, over all slots
     const int64_t kv_slot = (int64_t)(sq_slot / a.Hq) * a.Hkv + (sq_slot % a.Hq) / (a.Hq / a.Hkv);
     const int64_t r0 = (int64_t)rb * kM;
     const int64_t key_end = imin(a.m, r0 + kM);                      // keys any row here sees
@@ -521,8 +521,8 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_const
     __shared__ uint32_t tmem_slot;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sq_slot = blockIdx.y;                                  // (b, l, query head)
-    const int rb = gridDim.x - 1 - blockIdx.x;                       // longest blocks first
+    const int sq_slot = blockIdx.x;                                  // (b, l, query head)
+    const int rb = gridDim.y - 1 - blockIdx.y;                       // longest blocks first, over all slots
     const int64_t kv_slot = (int64_t)(sq_slot / a.Hq) * a.Hkv + (sq_slot % a.Hq) / (a.Hq / a.Hkv);
     const int64_t r0 = (int64_t)rb * 2 * kM;
     const bool two = r0 + kM < a.m;                                  // Q tile 1 has rows
@@ -869,14 +869,17 @@ cudaError_t launch_prefill_d(const PrefillArgs& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        dim3 grid((unsigned)((a.m + 2 * kM - 1) / (2 * kM)), (unsigned)q_slots);
+        // x = slot varies fastest in launch order, so every slot's longest
+        // (last) row block is issued before any shorter one: the causal work
+        // is scheduled longest first and the short blocks fill the tail
+        dim3 grid((unsigned)q_slots, (unsigned)((a.m + 2 * kM - 1) / (2 * kM)));
         prefill_pair_kernel<D><<<grid, kPairThreads, smem, st>>>(qmap, kmap, vmap, a);
         return cudaGetLastError();
     }
     const size_t smem = PL<D>::kBytes;
     cudaError_t e = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((a.m + kM - 1) / kM), (unsigned)q_slots);
+    dim3 grid((unsigned)q_slots, (unsigned)((a.m + kM - 1) / kM));
     prefill_kernel<D><<<grid, kThreads, smem, st>>>(qmap, kmap, vmap, a);
     return cudaGetLastError();
 }
