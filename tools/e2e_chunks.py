@@ -18,7 +18,10 @@ eng = VLCache(Shape(1, c["layers"], c["q_heads"], c["kv_heads"], c["head_dim"], 
               decode_steps=n_dec)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 st = torch.cuda.current_stream()
-for chunks, dec_chunks, early in [(4, 8, e_) for e_ in (0, 1, 2, 3, 8)] * 2:
+CASES = os.environ.get("E2E_CASES")   # "chunks,dec_chunks,early;..." (default: the dec_early sweep)
+grid = ([tuple(int(x) for x in c.split(",")) for c in CASES.split(";")] if CASES
+        else [(4, 8, e_) for e_ in (0, 1, 2, 3, 8)] * 2)
+for chunks, dec_chunks, early in grid:
     ts = []
     for i in range(8):
         flush.zero_()
