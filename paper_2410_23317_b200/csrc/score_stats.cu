@@ -299,6 +299,14 @@ cudaError_t launch_score_stats(const ScoreArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     e = launch_score_stats_tc(a, score_partials((int64_t)a.G * a.w), st);
     if (e != cudaSuccess || a.cap <= 0) return e;
+#ifdef VLC_FIX_PROBE   // timing probe (wrong results): 1 = no fix-up launches, 2 = fix_flags only
+    if (VLC_FIX_PROBE == 1) return cudaGetLastError();
+    if (VLC_FIX_PROBE == 2) {
+        e = a.d == 64 ? launch_pdl(fix_flags<64>, dim3(592), dim3(256), 0, st, a)
+                      : launch_pdl(fix_flags<128>, dim3(592), dim3(256), 0, st, a);
+        return e != cudaSuccess ? e : cudaGetLastError();
+    }
+#endif
     e = a.d == 64 ? launch_fixups<64>(a, st) : launch_fixups<128>(a, st);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
