@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libvlc_b200.so")
-SOURCES = ["vlc_api.cu", "score_stats.cu", "score_stats_tc.cu", "tma_host.cu", "budget.cu", "select.cu", "gather.cu", "decode.cu", "eval_rows.cu", "prefill.cu", "seam_f32.cu"]
+SOURCES = ["vlc_api.cu", "score_stats.cu", "score_stats_tc.cu", "tma_host.cu", "budget.cu", "select.cu", "gather.cu", "decode.cu", "decode_wide.cu", "eval_rows.cu", "prefill.cu", "seam_f32.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

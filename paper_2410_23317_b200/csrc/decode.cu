@@ -464,11 +464,28 @@ cudaError_t launch_d(const DecodeArgs& a, cudaStream_t st) {
 
 }  // namespace
 
-cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st) {
+#ifdef VLC_DEC_LAUNCH   // a second build of this file with another CTA shape (decode_wide.cu)
+cudaError_t VLC_DEC_LAUNCH(const DecodeArgs& a, cudaStream_t st) {
     if (a.G < 1 || a.G > kMaxG) return cudaErrorInvalidValue;
     if (a.d == 64) return launch_d<64>(a, st);
     if (a.d == 128) return launch_d<128>(a, st);
     return cudaErrorInvalidValue;
 }
+#else
+// Grids smaller than the GPU (fewer slots than SMs) gain nothing from small
+// CTAs -- no second step needs the room -- and each slot's stream is then the
+// whole step: they take the wide CTA (two-warp groups, 32-row tiles, 256
+// threads; decode_wide.cu).
+cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st) {
+    if (a.G < 1 || a.G > kMaxG) return cudaErrorInvalidValue;
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (a.slots < n_sm) return launch_decode_wide(a, st);
+    if (a.d == 64) return launch_d<64>(a, st);
+    if (a.d == 128) return launch_d<128>(a, st);
+    return cudaErrorInvalidValue;
+}
+#endif
 
 }  // namespace vlc

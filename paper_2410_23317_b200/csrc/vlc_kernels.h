@@ -141,6 +141,7 @@ struct DecodeArgs {
     int early;                 // set by the launcher: release the successor at once (see decode.cu)
 };
 cudaError_t launch_decode(const DecodeArgs& a, cudaStream_t st);
+cudaError_t launch_decode_wide(const DecodeArgs& a, cudaStream_t st);   // decode_wide.cu
 
 // f2: causal prefill attention over the prompt (prefill.cu).
 struct PrefillArgs {
