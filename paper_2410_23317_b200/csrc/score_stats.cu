@@ -278,6 +278,7 @@ int exact_ws_cap(int64_t bytes, int64_t slots, int64_t rows) {
 // the count outputs and exact mode's counters / row keys, zeroed in one launch
 __global__ void zero_outputs(unsigned* p0, int64_t n0, unsigned* p1, int64_t n1, unsigned* p2, int64_t n2,
                              unsigned* p3, int64_t n3) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // K1's prologue and pass 1 run under it
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1 + n2 + n3; i += stride) {
         if (i < n0) p0[i] = 0u;

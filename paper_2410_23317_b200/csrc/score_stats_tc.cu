@@ -25,6 +25,10 @@
 #include "sm100.cuh"
 #include "vlc_kernels.h"
 
+#ifndef VLC_K1_PDL
+#define VLC_K1_PDL 1   // launched under zero_outputs (programmatic dependent launch); waits before pass 2
+#endif
+
 namespace vlc {
 namespace {
 
@@ -358,6 +362,9 @@ score_stats_tc(const __grid_constant__ CUtensorMap qmap, const __grid_constant__
         //   below <=> u < t* log2e; mass = 2^(u - log2 S_r).  Serial per key: no
         //   cross-lane reduction, and every key column follows the same order.
         //   Each half writes its own partial row of col_partial (no barrier).
+        // the counters this pass accumulates into were zeroed by zero_outputs, the
+        // programmatic predecessor: everything before this point overlapped it
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int r0 = half * 64;
         const int64_t rg = r_first + r0;
         const bool one_head = rg / a.w == (rg + 63) / a.w;
@@ -502,8 +509,11 @@ cudaError_t launch_tc_e(const ScoreArgs& a, int nparts, cudaStream_t st) {
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int tail = units % n_sm;
     const int n_full = (VLC_K1_SPLIT_TAIL && tail > 0 && 2 * tail <= n_sm) ? units - tail : units;
-    score_stats_tc<D, EXACT><<<n_full + 2 * (units - n_full), kThreads, sm, st>>>(qmap, kmap, a, nparts, nblk, n_full);
-    return cudaGetLastError();
+    e = VLC_K1_PDL ? launch_pdl(score_stats_tc<D, EXACT>, dim3(n_full + 2 * (units - n_full)), dim3(kThreads), sm, st,
+                                qmap, kmap, a, nparts, nblk, n_full)
+                   : (score_stats_tc<D, EXACT><<<n_full + 2 * (units - n_full), kThreads, sm, st>>>(
+                          qmap, kmap, a, nparts, nblk, n_full), cudaSuccess);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int D>
