@@ -64,7 +64,7 @@ constexpr int kStages = VLC_DEC_STAGES;
 #define VLC_DEC_EARLYLAUNCH 1
 #endif
 #ifndef VLC_DEC_EARLY_PERIOD
-#define VLC_DEC_EARLY_PERIOD 16   // under early release, every P-th step releases late (bounds the deferred rows)
+#define VLC_DEC_EARLY_PERIOD 32   // under early release, every P-th step releases late (bounds the deferred rows)
 #endif
 #ifndef VLC_DEC_PROBE
 #define VLC_DEC_PROBE 0   // timing probes (wrong results), bits: 1 = no math, 2 = no TMA after the first ring, 4 = no wait for the previous step, 8 = no merge / output

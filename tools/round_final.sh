@@ -9,8 +9,8 @@ rm -f $O/sanitize_summary.txt
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_run.py > $O/sanitize_$tool.txt 2>&1
   echo "$tool rc=$?" >> $O/sanitize_summary.txt; tail -1 $O/sanitize_$tool.txt >> $O/sanitize_summary.txt
-  SAN_L=20 SAN_HKV=8 SAN_N=20 timeout 900 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_run.py > $O/sanitize_160x20_$tool.txt 2>&1
-  echo "160 slots x 20 steps $tool rc=$?" >> $O/sanitize_summary.txt; tail -1 $O/sanitize_160x20_$tool.txt >> $O/sanitize_summary.txt
+  SAN_L=20 SAN_HKV=8 SAN_N=40 timeout 900 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 9 python tools/sanitize_run.py > $O/sanitize_160x40_$tool.txt 2>&1
+  echo "160 slots x 40 steps $tool rc=$?" >> $O/sanitize_summary.txt; tail -1 $O/sanitize_160x40_$tool.txt >> $O/sanitize_summary.txt
 done
 cat $O/sanitize_summary.txt
 timeout 600 python bench.py > $O/bench_$TAG.json 2> $O/bench_$TAG.err
